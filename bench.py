@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""bench.py -- STAP datacubes/s on 1..N B200s (BASELINE.json metric), one JSON line.
+
+Workload: BASELINE.json configs[1] "STAP small" by
+default (4 channels, TDOF 3, 256 Doppler bins, 512 range cells, 16 steering
+vectors, training block 32); --config medium|large select configs[2]/[3].
+A step is one pass of the whole hot path (covariance + loading, Cholesky +
+solves -> MVDR weights, application) over a batch of `--cubes` distinct seeded
+synthetic datacubes resident in HBM (input > L2, so no L2 flush is needed).
+
+Multi-GPU (torchrun, one process per GPU, NCCL): Doppler-bin shards with weak
+scaling (BASELINE.json configs[4] pattern): the global cube has D = D_cfg x N
+bins, rank g owns the contiguous slice [g*D_cfg, (g+1)*D_cfg) plus a T-1 bin
+read-only halo, so per-GPU work is fixed; no collective is on the data path
+(--gather adds the optional NCCL all-gather of the outputs).  `value` counts
+every D_cfg-bin slice processed as one config-shaped datacube, summed over ranks.
+
+--impl reference times the fp64 C oracle (the reference arm for this tier) on
+the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOAD_DESC = {
+    "tiny": "STAP tiny (BASELINE.json configs[0])",
+    "small": "STAP small (BASELINE.json configs[1]): C=4, TDOF=3, D=256, R=512, S=16, K=32",
+    "medium": "STAP medium (BASELINE.json configs[2]): C=6, TDOF=5, D=512, R=1024, S=16, K=64",
+    "large": "STAP large (BASELINE.json configs[3]): C=8, TDOF=7, D=1024, R=4096, S=16, K=128",
+}
+DEFAULT_CUBES = {"tiny": 64, "small": 64, "medium": 16, "large": 2}
+
+
+# ---------------------------------------------------------------- algorithmic counts
+def counts(cfg: synth.StapConfig) -> dict:
+    """Per-cube algorithmic flops/bytes of the method.
+    cov_lag counts the Doppler-lag-shared covariance (the minimum work, what K1/K4 execute);
+    cov_bin the per-bin Hermitian count."""
+    C, T, D, R, K, S, N, B = cfg.C, cfg.T, cfg.D, cfg.R, cfg.K, cfg.S, cfg.N, cfg.B
+    X = D * C * R * 8
+    Y = S * D * R * 8
+    Rp = D * B * N * (N + 1) // 2 * 8
+    Wb = D * B * S * N * 8
+    Gb = D * B * S * 4
+    f = {
+        "cov_bin": 8.0 * D * R * N * (N + 1) / 2,
+        "cov_lag": 8.0 * D * R * (C * (C + 1) / 2 + (T - 1) * C * C),
+        "chol": (4.0 / 3.0) * N ** 3 * D * B,
+        "solve": 8.0 * N * N * S * D * B,
+        "apply": 8.0 * N * S * D * R,
+    }
+    return {
+        "flops_fused_lag": f["cov_lag"] + f["chol"] + f["solve"] + f["apply"],
+        "flops_fused_bin": f["cov_bin"] + f["chol"] + f["solve"] + f["apply"],
+        "bytes_fused": X + Y,
+        "stage": {
+            "covariance": {"flops": f["cov_lag"], "flops_bin": f["cov_bin"], "bytes": X + Rp},
+            "solve": {"flops": f["chol"] + f["solve"], "bytes": Rp + Wb + Gb},
+            "apply": {"flops": f["apply"], "bytes": X + Wb + Y},
+        },
+    }
+
+
+def peaks() -> dict:
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written) else the profiling guide's fallback.
+    FP32 SIMT peak = 148 SMs x 128 FP32 lanes x 2 flop x sm_max clock."""
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        p.update(hbm_gbs=float(m["hbm_gbs"]), sm_max_mhz=float(m.get("sm_max_mhz", 1965.0)),
+                 source="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        pass
+    p["fp32_tflops"] = 148 * 128 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    return p
+
+
+def roofline_obj(flops: float, nbytes: float, seconds: float, pk: dict, traffic=None, extra=None) -> dict:
+    t_alu = flops / (pk["fp32_tflops"] * 1e12)
+    t_hbm = nbytes / (pk["hbm_gbs"] * 1e9)
+    if t_alu >= t_hbm:
+        ach = flops / seconds / 1e12
+        o = {"bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+             "frac": ach / pk["fp32_tflops"]}
+    else:
+        ach = nbytes / seconds / 1e9
+        o = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
+    o["traffic"] = traffic
+    if extra:
+        o.update(extra)
+    return o
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [s for s in sm if s > 0.3 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- inputs
+def make_inputs(cfg, n_gpus, rank, cubes, steering_kind="ula"):
+    """This rank's cube buffers [cubes][D_cfg + halo][C][R] (halo only when N > 1), complex64."""
+    gcfg = cfg.with_(D=cfg.D * n_gpus) if n_gpus > 1 else cfg
+    lo, cnt = rank * cfg.D, cfg.D
+    b0, nb = synth.shard_window(gcfg, lo, cnt)
+    bins = (b0 + np.arange(nb)) % gcfg.D
+    x = np.empty((cubes, nb, cfg.C, cfg.R), np.complex64)
+    for i in range(cubes):
+        x[i] = synth.datacube_bins(gcfg, bins, cube_idx=i)
+    st = synth.steering(cfg, steering_kind)
+    return gcfg, lo, cnt, b0, nb, x, st
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def cpu_oracle_rate(cfg, budget_s: float, max_steps=None, sample_bins=None):
+    """Time the fp64 oracle (as it stands) on the host cores on a bounded sample; return
+    (cubes/s, cores, sample description, per-step seconds list)."""
+    import oracle
+    cores = oracle.max_threads()
+    bins = cfg.D if sample_bins is None else min(sample_bins, cfg.D)
+    d0 = cfg.D // 2 - bins // 2 if bins < cfg.D else 0
+    b0, nb = synth.shard_window(cfg, d0, bins)
+    local = synth.datacube_bins(cfg, (b0 + np.arange(nb)) % cfg.D, cube_idx=0)
+    st = synth.steering(cfg, "ula")
+    p = oracle.OracleParams(cfg.C, cfg.T, cfg.D, cfg.R, cfg.K, cfg.S, cfg.lam, dop_begin=d0, dop_count=bins,
+                            cube_bin0=b0, cube_bins=nb)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        oracle.run(p, local, st, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+        if max_steps is not None and len(times) >= max_steps:
+            break
+        if time.perf_counter() - t_start >= budget_s:
+            break
+    per = statistics.median(times)
+    rate = (bins / cfg.D) / per
+    sample = f"{bins} of {cfg.D} Doppler bins of one {cfg.name} cube per run, {len(times)} runs, fp64 C oracle, OpenMP over bins"
+    return rate, cores, sample, times
+
+
+def oracle_sample_bins(cfg):
+    # ~0.3-2 s per oracle call on a many-core host
+    return {"tiny": cfg.D, "small": cfg.D, "medium": 128, "large": 16}.get(cfg.name, cfg.D)
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    bins = oracle_sample_bins(cfg)
+    import oracle
+    cores = oracle.max_threads()
+    _, _, sample, _ = cpu_oracle_rate(cfg, 0.0, max_steps=max(1, args.warmup), sample_bins=bins)
+    rate, cores, sample, times = cpu_oracle_rate(cfg, 1e9, max_steps=args.steps, sample_bins=bins)
+    ms = statistics.median(times) * 1e3
+    line = {
+        "impl": "reference", "metric": "STAP datacubes/sec", "value": rate, "unit": "cubes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_obj(args, cfg, world),
+        "cpu_baseline": {"value": rate, "unit": "cubes/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": rate, "unit": "cubes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_obj(args, cfg, world):
+    return {"workload": WORKLOAD_DESC.get(cfg.name, cfg.name), "C": cfg.C, "TDOF": cfg.T, "D": cfg.D, "R": cfg.R,
+            "S": cfg.S, "K": cfg.K, "lambda": cfg.lam, "cubes_per_step_per_gpu": args.cubes,
+            "parallelism": f"doppler-shard x{world} (weak: global D = {cfg.D}*{world})",
+            "l2": "inputs larger than L2 (no flush)", "steering": "ULA centre-bin"}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(WORKLOAD_DESC), default="small")
+    ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
+    ap.add_argument("--path", choices=["auto", "staged"], default="auto")
+    ap.add_argument("--gather", action="store_true", help="NCCL all-gather of outputs after each step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stages", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.config]
+    if args.cubes is None:
+        args.cubes = DEFAULT_CUBES[args.config]
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = max(world, 1)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2203_06233_b200 as stap
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes)
+    M = args.cubes
+    dims = stap.Dims(cfg.C, cfg.T, gcfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
+    plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
+                         device=local_rank)
+    stream = torch.cuda.current_stream(dev)
+    cube = torch.from_numpy(x_h).to(dev)
+    steer = torch.from_numpy(st_h).to(dev)
+    out = torch.empty(plan.out_shape, dtype=torch.complex64, device=dev)
+    info = torch.empty(plan.info_shape, dtype=torch.int32, device=dev)
+    staged = args.path == "staged" or plan.description.startswith("staged")
+    if staged:
+        cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=dev)
+        wts = torch.empty(plan.weights_shape, dtype=torch.complex64, device=dev)
+        gam = torch.empty(plan.info_shape + (cfg.S,), dtype=torch.float32, device=dev)
+    ws = plan.workspace()
+    gather_buf = None
+    if args.gather and world > 1:
+        gather_buf = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
+    s_ = stap._stream(stream, local_rank)
+
+    ev_stage = []
+
+    def step(record=False):
+        if staged:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
+            if record:
+                e[0].record(stream)
+            stap.stap_covariance(plan.handle, cube, cov, s_)
+            if record:
+                e[1].record(stream)
+            stap.stap_solve_weights(plan.handle, cov, steer, wts, gam, info, s_)
+            if record:
+                e[2].record(stream)
+            stap.stap_apply(plan.handle, cube, wts, out, s_)
+            if record:
+                e[3].record(stream)
+                ev_stage.append(e)
+        else:
+            stap.stap_run(plan.handle, cube, steer, out, info, ws, plan.workspace_bytes, s_)
+        if gather_buf is not None:
+            dist.all_gather_into_tensor(gather_buf.view(-1), out.view(-1))
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=staged)
+        t1.record(stream)
+        barrier()
+    elapsed = t0.elapsed_time(t1) / 1e3
+    tmax = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed = float(tmax.item())
+    cubes_total = world * M * args.steps
+    value = cubes_total / elapsed
+    ms_per_step = elapsed / args.steps * 1e3
+    ninfo_bad = int((info != 0).sum().item())
+
+    pk = peaks()
+    cnt_cfg = counts(cfg)
+    launches_per_step = 3 if staged else 1
+    if staged:
+        dur = {k: [] for k in ("covariance", "solve", "apply")}
+        for e in ev_stage:
+            dur["covariance"].append(e[0].elapsed_time(e[1]) / 1e3)
+            dur["solve"].append(e[1].elapsed_time(e[2]) / 1e3)
+            dur["apply"].append(e[2].elapsed_time(e[3]) / 1e3)
+        avg = {k: sum(v) / len(v) for k, v in dur.items()}
+        top = max(avg, key=avg.get)
+        sc = cnt_cfg["stage"][top]
+        roof = roofline_obj(sc["flops"] * M, sc["bytes"] * M, avg[top], pk,
+                            extra={"kernel": top, "share_of_step": avg[top] / (elapsed / args.steps)})
+    else:
+        t_launch = elapsed / args.steps
+        roof = roofline_obj(cnt_cfg["flops_fused_lag"] * M, cnt_cfg["bytes_fused"] * M, t_launch, pk,
+                            extra={"kernel": "fused_kernel (stap_run)", "share_of_step": 1.0,
+                                   "achieved_perbin_count": cnt_cfg["flops_fused_bin"] * M / t_launch / 1e12})
+    roof["peak_source"] = pk["source"]
+
+    result = {
+        "metric": "STAP datacubes/sec", "value": value, "unit": "cubes/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_obj(args, cfg, world),
+        "path": plan.description, "gpu_launches": launches_per_step * args.steps, "roofline": roof,
+        "clocks": clk.summary(), "info_nonzero": ninfo_bad,
+    }
+
+    # per-stage roofline fractions (BASELINE.json metric: "% of HBM/FP32 roofline per stage")
+    if not args.no_stages:
+        result["stages"] = stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, local_rank)
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    if not args.no_e2e:
+        result["e2e"] = e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample, _ = cpu_oracle_rate(cfg, args.cpu_budget, sample_bins=oracle_sample_bins(cfg))
+        result["cpu_baseline"] = {"value": rate, "unit": "cubes/s", "cores": cores, "kind": "oracle",
+                                  "sample": sample}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+        dist.destroy_process_group()
+
+
+def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
+    import torch
+    s_ = stap._stream(stream, dev_idx)
+    cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=cube.device)
+    wts = torch.empty(plan.weights_shape, dtype=torch.complex64, device=cube.device)
+    gam = torch.empty(plan.info_shape + (cfg.S,), dtype=torch.float32, device=cube.device)
+    info = torch.empty(plan.info_shape, dtype=torch.int32, device=cube.device)
+    out = torch.empty(plan.out_shape, dtype=torch.complex64, device=cube.device)
+    fns = {
+        "covariance": lambda: stap.stap_covariance(plan.handle, cube, cov, s_),
+        "solve": lambda: stap.stap_solve_weights(plan.handle, cov, steer, wts, gam, info, s_),
+        "apply": lambda: stap.stap_apply(plan.handle, cube, wts, out, s_),
+    }
+    c = counts(cfg)["stage"]
+    res = {}
+    for name, fn in fns.items():
+        fn()
+    torch.cuda.synchronize()
+    for name, fn in fns.items():
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / reps
+        r = roofline_obj(c[name]["flops"] * M, c[name]["bytes"] * M, t, pk)
+        res[name] = {"us": t * 1e6, "bound": r["bound"], "achieved": r["achieved"], "unit": r["unit"],
+                     "frac": r["frac"]}
+    return res
+
+
+def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
+    import torch
+    hc = torch.from_numpy(x_h).pin_memory()
+    hs = torch.from_numpy(st_h).pin_memory()
+    ho = torch.empty(plan.out_shape, dtype=torch.complex64).pin_memory()
+    hi = torch.empty(plan.info_shape, dtype=torch.int32).pin_memory()
+    ws = torch.empty(max(plan.host_workspace_bytes, 16), dtype=torch.uint8, device=dev)
+    steps = max(1, min(args.steps, 5))
+    for _ in range(2):
+        plan.run_host(hc, hs, ho, hi, ws, stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        plan.run_host(hc, hs, ho, hi, ws, stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    h2d = hc.numel() * 8 + hs.numel() * 8
+    d2h = ho.numel() * 8 + hi.numel() * 4
+    return {"value": world * M * steps / t, "unit": "cubes/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "api": "stap_run_host (pinned host buffers)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * include/stap.h -- C ABI of libstap.so, the B200 (sm_100a) STAP hot path.
+ *
+ * What the library computes (BASELINE.json north_star; the paper itself never
+ * states the STAP mathematics, so every convention is a DESIGN.md "reading"):
+ *
+ *   datacube X[D][C][R] complex64: Doppler bins x channels x range cells, i.e.
+ *     the paper's "# pulses per cube, # channels, # samples per pulse"
+ *     (sec. 5.3) after the per-row Doppler FFT (PAPER.md:340,
+ *     Table 2 row "fft_2D,axis=1"); readings c-1, c-14.
+ *   unit (d, b): Doppler bin d, training block b = range cells [bK, bK+K)
+ *     (reading c-7); units are independent -- the outer parallel loop of
+ *     PAPER.md:420-430 (Fig. 7 text) and PAPER.md:408-418.
+ *   snapshot z_{d,r}[t*C + c] = X[(d - h + t) mod D][c][r], h = floor((T-1)/2)
+ *     (readings c-2, c-3, c-4).
+ *   stap_covariance    : R_{d,b} = (1/K) sum_{r in b} z z^H + delta I,
+ *                        delta = lambda tr(Rhat)/N            (c-5, c-6)
+ *   stap_solve_weights : R = L L^H (Cholesky), y_k = L^-1 s_k, gamma_k = ||y_k||^2,
+ *                        w_k = L^-H y_k / gamma_k  (MVDR, w_k^H s_k = 1)  (c-9, c-10)
+ *   stap_apply         : Y[d][k][r] = w_{d,b(r),k}^H z_{d,r}     (c-12)
+ *   stap_run           : all of the above, fused, cube in -> Y out.
+ *
+ * Conventions (all entry points):
+ *  - Layouts are row-major, last index fastest.  complex64 = {float re, im}
+ *    interleaved (== torch.complex64 == cuFloatComplex).
+ *  - Device pointers must be 16-byte aligned device memory of the plan's
+ *    device; the caller owns every buffer; inputs are const and never written.
+ *  - Every call only enqueues work on `stream` and returns (no host sync, no
+ *    allocation), so calls are CUDA-graph capturable -- except stap_run_host,
+ *    which also enqueues the host<->device copies.  Argument errors are
+ *    returned synchronously and NOTHING is launched.  Numerical failures are
+ *    reported on the device in `info` (reading c-11):
+ *        0       the unit is fine
+ *        j > 0   Cholesky pivot j (1-based) was <= 0 or not finite: every
+ *                weight and output of that unit is 0
+ *        -(k+1)  gamma_k <= 0 or not finite for the smallest such k: the
+ *                weights/outputs of every failing k are 0.
+ *  - Arithmetic is FP32 (no TF32, no fast-math); results match the fp64 oracle
+ *    to the tolerances in DESIGN.md, not bitwise.  A given plan computes every
+ *    unit with a fixed summation order that does not depend on dop_begin,
+ *    dop_count or batch: shards are bitwise identical to the unsharded run.
+ *  - There is no CPU fallback: without an sm_100 device every call fails.
+ */
+#ifndef STAP_H_
+#define STAP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STAP_ABI_VERSION 1
+
+typedef struct { float re, im; } stap_c64;
+typedef struct stap_plan stap_plan;
+
+typedef enum {
+    STAP_OK = 0,
+    STAP_ERR_NULL_ARG = 1,     /* a required pointer is NULL */
+    STAP_ERR_BAD_DIMS = 2,     /* a dim <= 0, R % K != 0, T > D, shard or cube window
+                                  out of range, lambda < 0 or not finite, workspace too small */
+    STAP_ERR_UNSUPPORTED = 3,  /* valid but not implemented: N = C*T > 64, S > 32, K odd,
+                                  K > 1024, C > 8 */
+    STAP_ERR_MISALIGNED = 4,   /* a device pointer is not 16-byte aligned */
+    STAP_ERR_CUDA = 5,         /* a CUDA runtime / launch error */
+    STAP_ERR_DEVICE = 7        /* no device, or the plan's device is not sm_100 */
+} stap_status;
+
+typedef struct {
+    int32_t n_chan;          /* C  channels                      ("# channels") */
+    int32_t tdof;            /* T  temporal DOF: adjacent Doppler bins per snapshot (north_star) */
+    int32_t n_dop;           /* D  Doppler bins, global          ("# pulses per cube") */
+    int32_t n_range;         /* R  range cells                   ("# samples per pulse") */
+    int32_t training_block;  /* K  range cells per training block; R % K == 0 (north_star) */
+    int32_t n_steering;      /* S  steering vectors              (north_star) */
+    float   diag_load;       /* lambda >= 0, delta = lambda tr(Rhat)/N (reading c-6) */
+    int32_t dop_begin;       /* first owned Doppler bin (0 on one GPU)                    */
+    int32_t dop_count;       /* owned bins D_loc (n_dop on one GPU)                        */
+    int32_t cube_bin0;       /* global bin held in row 0 of the cube buffer               */
+    int32_t cube_bins;       /* bins held by the cube buffer (n_dop = the whole cube); the
+                                buffer holds bins cube_bin0 .. cube_bin0+cube_bins-1 mod D
+                                and must cover every owned bin's window                   */
+    int32_t batch;           /* independent cubes per call (>= 1), stored back to back     */
+    int32_t device;          /* CUDA ordinal the plan launches on                          */
+} stap_params;
+
+/* Buffer shapes (complex64 unless noted), with B = R/K, N = C*T, Dl = dop_count:
+ *   cube     [batch][cube_bins][C][R]
+ *   steering [S][N]                    (element i = t*C + c; shared by every unit)
+ *   cov      [batch][Dl][B][N][N]      (full Hermitian, loading applied)
+ *   weights  [batch][Dl][B][S][N]
+ *   gamma    [batch][Dl][B][S]   float (nullable)
+ *   info     [batch][Dl][B]      int32
+ *   out      [batch][Dl][S][R]     (Doppler-major: shard g starts at dop_begin*S*R) */
+
+/* Validate `p` and build an immutable plan (host metadata only). */
+stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan);
+/* Legal once all work using the plan has completed. NULL is accepted. */
+stap_status stap_plan_destroy(stap_plan* plan);
+/* Device workspace stap_run (host_io = 0) or stap_run_host (host_io = 1) needs. */
+stap_status stap_plan_workspace_bytes(const stap_plan* plan, int32_t host_io, size_t* bytes);
+/* Kernel the plan selected for stap_run ("fused:..." or "staged:..."), for logs. */
+const char* stap_plan_describe(const stap_plan* plan);
+
+/* Stage 1: loaded covariance of every owned unit.  Reads only the bins each window needs. */
+stap_status stap_covariance(const stap_plan* plan, const stap_c64* cube, stap_c64* cov,
+                            cudaStream_t stream);
+/* Stage 2: Cholesky + forward/back solves -> MVDR weights, gamma, info. */
+stap_status stap_solve_weights(const stap_plan* plan, const stap_c64* cov, const stap_c64* steering,
+                               stap_c64* weights, float* gamma, int32_t* info, cudaStream_t stream);
+/* Stage 3: Y = W^H z for every owned bin and range cell. */
+stap_status stap_apply(const stap_plan* plan, const stap_c64* cube, const stap_c64* weights,
+                       stap_c64* out, cudaStream_t stream);
+/* Whole path.  `workspace` (device, >= stap_plan_workspace_bytes(plan, 0, .) bytes,
+ * may be NULL when that is 0) holds intermediates when the plan is staged. */
+stap_status stap_run(const stap_plan* plan, const stap_c64* cube, const stap_c64* steering,
+                     stap_c64* out, int32_t* info, void* workspace, size_t workspace_bytes,
+                     cudaStream_t stream);
+/* Whole path from HOST buffers (pinned for async copies): enqueues H2D of cube and
+ * steering, stap_run, and D2H of out and info, all on `stream`; the caller
+ * synchronises the stream before reading h_out / h_info.  Device staging lives
+ * in `workspace` (>= stap_plan_workspace_bytes(plan, 1, .)). */
+stap_status stap_run_host(const stap_plan* plan, const stap_c64* h_cube, const stap_c64* h_steering,
+                          stap_c64* h_out, int32_t* h_info, void* workspace, size_t workspace_bytes,
+                          cudaStream_t stream);
+
+const char* stap_status_string(stap_status s);
+int32_t stap_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STAP_H_ */

@@ -1,0 +1,292 @@
+"""paper_2203_06233_b200 -- B200-native STAP hot path (arXiv 2203.06233, sec. 5.3).
+
+A thin ctypes binding over ``libstap.so`` (include/stap.h).  Every step of the
+path -- covariance with diagonal loading, Cholesky + forward/back solves giving
+the MVDR weights, and weight application -- runs in the library's sm_100a
+kernels; this module only marshals arguments (torch tensors supply device
+memory and streams).  There is no CPU fallback: importing the package fails
+loudly if the extension has not been built.
+
+Entry points mirror the C ABI names: ``stap_plan_create``, ``stap_covariance``,
+``stap_solve_weights``, ``stap_apply``, ``stap_run``, ``stap_run_host``,
+``stap_plan_workspace_bytes``; ``StapPlan`` wraps them with shape checks.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstap.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA extension first "
+        "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = {0: "STAP_OK", 1: "STAP_ERR_NULL_ARG", 2: "STAP_ERR_BAD_DIMS", 3: "STAP_ERR_UNSUPPORTED",
+          4: "STAP_ERR_MISALIGNED", 5: "STAP_ERR_CUDA", 7: "STAP_ERR_DEVICE"}
+
+SYMBOLS = ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_plan_describe",
+           "stap_covariance", "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host",
+           "stap_status_string", "stap_abi_version")
+
+
+class StapError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        msg = _lib.stap_status_string(code).decode()
+        super().__init__(f"{what}: {msg}")
+
+
+class stap_params(ctypes.Structure):
+    _fields_ = [
+        ("n_chan", ctypes.c_int32), ("tdof", ctypes.c_int32), ("n_dop", ctypes.c_int32),
+        ("n_range", ctypes.c_int32), ("training_block", ctypes.c_int32), ("n_steering", ctypes.c_int32),
+        ("diag_load", ctypes.c_float), ("dop_begin", ctypes.c_int32), ("dop_count", ctypes.c_int32),
+        ("cube_bin0", ctypes.c_int32), ("cube_bins", ctypes.c_int32), ("batch", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+    ]
+
+
+_vp = ctypes.c_void_p
+_P = ctypes.POINTER(stap_params)
+_lib.stap_plan_create.argtypes = [_P, ctypes.POINTER(_vp)]
+_lib.stap_plan_destroy.argtypes = [_vp]
+_lib.stap_plan_workspace_bytes.argtypes = [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+_lib.stap_plan_describe.argtypes = [_vp]
+_lib.stap_plan_describe.restype = ctypes.c_char_p
+_lib.stap_covariance.argtypes = [_vp, _vp, _vp, _vp]
+_lib.stap_solve_weights.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.stap_apply.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.stap_run.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+_lib.stap_run_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+_lib.stap_status_string.argtypes = [ctypes.c_int]
+_lib.stap_status_string.restype = ctypes.c_char_p
+_lib.stap_abi_version.restype = ctypes.c_int32
+for _f in ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_covariance",
+           "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise StapError(rc, what)
+
+
+def _ptr(t) -> _vp:
+    if t is None:
+        return _vp(0)
+    if isinstance(t, int):
+        return _vp(t)
+    return _vp(t.data_ptr())
+
+
+def _stream(stream, device: int) -> _vp:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return _vp(stream.cuda_stream)
+
+
+# ---------------------------------------------------------------- raw C-ABI mirrors
+def stap_abi_version() -> int:
+    return int(_lib.stap_abi_version())
+
+
+def stap_status_string(code: int) -> str:
+    return _lib.stap_status_string(code).decode()
+
+
+def stap_plan_create(params: stap_params) -> int:
+    h = _vp()
+    _check(_lib.stap_plan_create(ctypes.byref(params), ctypes.byref(h)), "stap_plan_create")
+    return h.value
+
+
+def stap_plan_destroy(plan: int) -> None:
+    _check(_lib.stap_plan_destroy(_vp(plan)), "stap_plan_destroy")
+
+
+def stap_plan_workspace_bytes(plan: int, host_io: bool = False) -> int:
+    n = ctypes.c_size_t()
+    _check(_lib.stap_plan_workspace_bytes(_vp(plan), int(host_io), ctypes.byref(n)), "stap_plan_workspace_bytes")
+    return int(n.value)
+
+
+def stap_plan_describe(plan: int) -> str:
+    return _lib.stap_plan_describe(_vp(plan)).decode()
+
+
+def stap_covariance(plan: int, cube, cov, stream) -> None:
+    _check(_lib.stap_covariance(_vp(plan), _ptr(cube), _ptr(cov), stream), "stap_covariance")
+
+
+def stap_solve_weights(plan: int, cov, steering, weights, gamma, info, stream) -> None:
+    _check(_lib.stap_solve_weights(_vp(plan), _ptr(cov), _ptr(steering), _ptr(weights), _ptr(gamma),
+                                   _ptr(info), stream), "stap_solve_weights")
+
+
+def stap_apply(plan: int, cube, weights, out, stream) -> None:
+    _check(_lib.stap_apply(_vp(plan), _ptr(cube), _ptr(weights), _ptr(out), stream), "stap_apply")
+
+
+def stap_run(plan: int, cube, steering, out, info, workspace, workspace_bytes: int, stream) -> None:
+    _check(_lib.stap_run(_vp(plan), _ptr(cube), _ptr(steering), _ptr(out), _ptr(info), _ptr(workspace),
+                         workspace_bytes, stream), "stap_run")
+
+
+def stap_run_host(plan: int, h_cube, h_steering, h_out, h_info, workspace, workspace_bytes: int, stream) -> None:
+    _check(_lib.stap_run_host(_vp(plan), _ptr(h_cube), _ptr(h_steering), _ptr(h_out), _ptr(h_info),
+                              _ptr(workspace), workspace_bytes, stream), "stap_run_host")
+
+
+# ---------------------------------------------------------------- convenience wrapper
+@dataclass
+class Dims:
+    """Dimensions in the paper's vocabulary (PAPER.md:604-605 + north_star)."""
+    C: int
+    T: int
+    D: int
+    R: int
+    K: int
+    S: int
+    lam: float = 1e-2
+
+    @property
+    def N(self) -> int:
+        return self.C * self.T
+
+    @property
+    def B(self) -> int:
+        return self.R // self.K
+
+
+class StapPlan:
+    """Owns a libstap plan; methods take torch tensors on the plan's device."""
+
+    def __init__(self, dims: Dims, dop_begin: int = 0, dop_count: int | None = None, cube_bin0: int = 0,
+                 cube_bins: int | None = None, batch: int = 1, device: int = 0):
+        self.dims = dims
+        self.dop_begin = dop_begin
+        self.dop_count = dims.D if dop_count is None else dop_count
+        self.cube_bin0 = cube_bin0
+        self.cube_bins = dims.D if cube_bins is None else cube_bins
+        self.batch = batch
+        self.device = device
+        self.params = stap_params(dims.C, dims.T, dims.D, dims.R, dims.K, dims.S, float(dims.lam), dop_begin,
+                                  self.dop_count, cube_bin0, self.cube_bins, batch, device)
+        self.handle = stap_plan_create(self.params)
+        self.workspace_bytes = stap_plan_workspace_bytes(self.handle, False)
+        self.host_workspace_bytes = stap_plan_workspace_bytes(self.handle, True)
+        self.description = stap_plan_describe(self.handle)
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            _lib.stap_plan_destroy(_vp(h))
+            self.handle = None
+
+    # shapes ------------------------------------------------------------
+    @property
+    def cube_shape(self):
+        d = self.dims
+        return (self.batch, self.cube_bins, d.C, d.R)
+
+    @property
+    def out_shape(self):
+        d = self.dims
+        return (self.batch, self.dop_count, d.S, d.R)
+
+    @property
+    def cov_shape(self):
+        d = self.dims
+        return (self.batch, self.dop_count, d.B, d.N, d.N)
+
+    @property
+    def weights_shape(self):
+        d = self.dims
+        return (self.batch, self.dop_count, d.B, d.S, d.N)
+
+    @property
+    def info_shape(self):
+        return (self.batch, self.dop_count, self.dims.B)
+
+    def _chk(self, t, shape, dtype, name):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch tensor")
+        if t.dtype != dtype or not t.is_contiguous() or t.device != torch.device("cuda", self.device):
+            raise ValueError(f"{name}: need contiguous {dtype} on cuda:{self.device}, got {t.dtype} on {t.device}")
+        if tuple(t.shape) != tuple(shape) and t.numel() != _numel(shape):
+            raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+
+    # stages ------------------------------------------------------------
+    def covariance(self, cube, cov=None, stream=None):
+        import torch
+        self._chk(cube, self.cube_shape, torch.complex64, "cube")
+        if cov is None:
+            cov = torch.empty(self.cov_shape, dtype=torch.complex64, device=cube.device)
+        self._chk(cov, self.cov_shape, torch.complex64, "cov")
+        stap_covariance(self.handle, cube, cov, _stream(stream, self.device))
+        return cov
+
+    def solve_weights(self, cov, steering, weights=None, gamma=None, info=None, stream=None):
+        import torch
+        d = self.dims
+        self._chk(cov, self.cov_shape, torch.complex64, "cov")
+        self._chk(steering, (d.S, d.N), torch.complex64, "steering")
+        dev = cov.device
+        if weights is None:
+            weights = torch.empty(self.weights_shape, dtype=torch.complex64, device=dev)
+        if gamma is None:
+            gamma = torch.empty(self.info_shape + (d.S,), dtype=torch.float32, device=dev)
+        if info is None:
+            info = torch.empty(self.info_shape, dtype=torch.int32, device=dev)
+        stap_solve_weights(self.handle, cov, steering, weights, gamma, info, _stream(stream, self.device))
+        return weights, gamma, info
+
+    def apply(self, cube, weights, out=None, stream=None):
+        import torch
+        self._chk(cube, self.cube_shape, torch.complex64, "cube")
+        self._chk(weights, self.weights_shape, torch.complex64, "weights")
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.complex64, device=cube.device)
+        stap_apply(self.handle, cube, weights, out, _stream(stream, self.device))
+        return out
+
+    def workspace(self):
+        import torch
+        if self._ws is None or self._ws.numel() < max(self.workspace_bytes, 1):
+            self._ws = torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def run(self, cube, steering, out=None, info=None, stream=None):
+        import torch
+        d = self.dims
+        self._chk(cube, self.cube_shape, torch.complex64, "cube")
+        self._chk(steering, (d.S, d.N), torch.complex64, "steering")
+        dev = cube.device
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.complex64, device=dev)
+        if info is None:
+            info = torch.empty(self.info_shape, dtype=torch.int32, device=dev)
+        ws = self.workspace()
+        stap_run(self.handle, cube, steering, out, info, ws, self.workspace_bytes, _stream(stream, self.device))
+        return out, info
+
+    def run_host(self, h_cube, h_steering, h_out, h_info, workspace, stream=None):
+        """Host buffers (pinned torch CPU tensors) in and out; caller synchronises `stream`."""
+        stap_run_host(self.handle, h_cube, h_steering, h_out, h_info, workspace, self.host_workspace_bytes,
+                      _stream(stream, self.device))
+
+
+def _numel(shape):
+    n = 1
+    for s in shape:
+        n *= s
+    return n

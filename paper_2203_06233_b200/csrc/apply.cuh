@@ -1,0 +1,88 @@
+// apply.cuh -- K3: Y[d][k][r] = w_{d,b(r),k}^H z_{d,r} for every owned bin and range cell.
+//
+// Method (include/stap.h; reading c-12): z_{d,r}[t*C + c] = X[(d-h+t) mod D][c][r].
+//
+// Design: every snapshot element is used by exactly one output column (all S
+// weights of its unit), so the cube is streamed straight from HBM with
+// coalesced 16-byte loads (2 consecutive range cells per thread) and never
+// staged; the unit's weights -- shared by all threads of the unit -- are
+// staged in shared memory transposed to [i][k] so that the S weights of one
+// snapshot element are read with broadcast float4 loads.  A thread keeps
+// SMAX x 2 complex accumulators; stores are 16-byte, coalesced along r.
+#pragma once
+#include "common.cuh"
+
+namespace stapk {
+
+__host__ inline int apply_tpu(int K) { return K / 2 < 128 ? K / 2 : 128; }  // threads per unit
+__host__ inline size_t apply_smem_bytes(int N, int SMAX, int units_per_cta) {
+  return (size_t)units_per_cta * N * SMAX * 8;
+}
+
+// grid.x over groups of `upc` units (unit = ((n*Dl + dl)*B + b)); blockDim = upc * tpu.
+template <int SMAX>
+__global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __restrict__ cube,
+                                                     const float2* __restrict__ wts,
+                                                     float2* __restrict__ out, int tpu, int upc,
+                                                     long long units) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int N = p.N, S = p.S, K = p.K, C = p.C;
+  float2* Wt = reinterpret_cast<float2*>(smem);  // [upc][N][SMAX]
+  const int tid = threadIdx.x;
+  const long long u0 = (long long)blockIdx.x * upc;
+
+  // stage weights, transposed, zero-padded to SMAX
+  for (int idx = tid; idx < upc * N * SMAX; idx += blockDim.x) {
+    const int uu = idx / (N * SMAX);
+    const int rem = idx - uu * N * SMAX;
+    const int i = rem / SMAX, k = rem - i * SMAX;
+    float2 v = make_float2(0.f, 0.f);
+    if (u0 + uu < units && k < S) v = wts[(u0 + uu) * S * N + (long long)k * N + i];
+    Wt[idx] = v;
+  }
+  __syncthreads();
+
+  const int uu = tid / tpu, tp = tid - uu * tpu;
+  const long long u = u0 + uu;
+  if (uu >= upc || u >= units) return;
+  const int b = (int)(u % p.B);
+  const long long nd = u / p.B;  // n*Dl + dl
+  const int dl = (int)(nd % p.dop_count);
+  const int n = (int)(nd / p.dop_count);
+  const int d = p.dop_begin + dl;
+  const float2* w_s = Wt + (size_t)uu * N * SMAX;
+  const float2* cb = cube + (long long)n * p.cube_stride + (long long)b * K;
+  float2* yb = out + (((long long)n * p.dop_count + dl) * S) * p.R + (long long)b * K;
+
+  for (int jp = tp; jp < K / 2; jp += tpu) {
+    const int j = 2 * jp;
+    float2 acc0[SMAX], acc1[SMAX];
+#pragma unroll
+    for (int k = 0; k < SMAX; ++k) acc0[k] = acc1[k] = make_float2(0.f, 0.f);
+    int i = 0;
+    for (int t = 0; t < p.T; ++t) {
+      const int lb = local_bin(p, d - p.h + t);
+      const float2* row = cb + (long long)lb * C * p.R + j;
+      for (int c = 0; c < C; ++c, ++i) {
+        const float4 z = __ldg(reinterpret_cast<const float4*>(row + (long long)c * p.R));
+        const float2 z0 = make_float2(z.x, z.y), z1 = make_float2(z.z, z.w);
+        const float4* wv = reinterpret_cast<const float4*>(w_s + i * SMAX);
+#pragma unroll
+        for (int k2 = 0; k2 < SMAX / 2; ++k2) {
+          const float4 ww = wv[k2];
+          cmac_conja(acc0[2 * k2], make_float2(ww.x, ww.y), z0);
+          cmac_conja(acc1[2 * k2], make_float2(ww.x, ww.y), z1);
+          cmac_conja(acc0[2 * k2 + 1], make_float2(ww.z, ww.w), z0);
+          cmac_conja(acc1[2 * k2 + 1], make_float2(ww.z, ww.w), z1);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SMAX; ++k)
+      if (k < S)
+        *reinterpret_cast<float4*>(yb + (long long)k * p.R + j) =
+            make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y);
+  }
+}
+
+}  // namespace stapk

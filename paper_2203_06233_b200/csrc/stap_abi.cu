@@ -1,0 +1,399 @@
+// stap_abi.cu -- host side of libstap.so: plan validation, launch-shape
+// selection and the extern "C" entry points declared in include/stap.h.
+//
+// Nothing here does arithmetic of the method; every step runs in the kernels
+// of cov.cuh (K1), solve.cuh (K2), apply.cuh (K3) and fused.cuh (K4).  There
+// is no CPU path: without an sm_100 device every call returns an error.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/stap.h"
+#include "apply.cuh"
+#include "cov.cuh"
+#include "fused.cuh"
+#include "solve.cuh"
+
+using namespace stapk;
+
+struct stap_plan {
+  stap_params prm;
+  KParams kp;
+  long long units;  // batch * dop_count * B
+  // K1
+  int cov_P, cov_threads, cov_runs;
+  size_t cov_smem;
+  // K2
+  int solve_wpc, solve_grid;
+  size_t solve_smem;
+  // K3
+  int apply_tpu, apply_upc, apply_smax, apply_grid;
+  size_t apply_smem;
+  // K4 (fused) selection
+  int fused;  // 1 if stap_run uses the fused kernel
+  FusedCfg fcfg;
+  // staged workspace layout
+  size_t ws_cov, ws_w, ws_g, ws_total;
+  size_t cube_bytes, steer_bytes, out_bytes, info_bytes;
+  char desc[160];
+};
+
+namespace {
+
+const size_t kSmemCap = 227 * 1024;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) return;
+    ok = true;
+  }
+  ~DeviceGuard() {
+    if (ok && prev >= 0) {
+      int cur = -1;
+      if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+  }
+};
+
+template <int C>
+void cov_attr(size_t smem) {
+  cudaFuncSetAttribute(cov_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t set_cov_attr(int C, size_t smem) {
+  switch (C) {
+    case 1: cov_attr<1>(smem); break;
+    case 2: cov_attr<2>(smem); break;
+    case 3: cov_attr<3>(smem); break;
+    case 4: cov_attr<4>(smem); break;
+    case 5: cov_attr<5>(smem); break;
+    case 6: cov_attr<6>(smem); break;
+    case 7: cov_attr<7>(smem); break;
+    case 8: cov_attr<8>(smem); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int C>
+void cov_launch_t(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
+  dim3 grid(pl->cov_runs, pl->kp.B, pl->kp.batch);
+  cov_kernel<C><<<grid, pl->cov_threads, pl->cov_smem, st>>>(pl->kp, cube, cov, pl->cov_P);
+}
+
+void cov_launch(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
+  switch (pl->kp.C) {
+    case 1: cov_launch_t<1>(pl, cube, cov, st); break;
+    case 2: cov_launch_t<2>(pl, cube, cov, st); break;
+    case 3: cov_launch_t<3>(pl, cube, cov, st); break;
+    case 4: cov_launch_t<4>(pl, cube, cov, st); break;
+    case 5: cov_launch_t<5>(pl, cube, cov, st); break;
+    case 6: cov_launch_t<6>(pl, cube, cov, st); break;
+    case 7: cov_launch_t<7>(pl, cube, cov, st); break;
+    case 8: cov_launch_t<8>(pl, cube, cov, st); break;
+  }
+}
+
+template <int SMAX>
+void apply_launch_t(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
+  apply_kernel<SMAX><<<pl->apply_grid, pl->apply_upc * pl->apply_tpu, pl->apply_smem, st>>>(
+      pl->kp, cube, w, out, pl->apply_tpu, pl->apply_upc, pl->units);
+}
+
+void apply_launch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
+  switch (pl->apply_smax) {
+    case 2: apply_launch_t<2>(pl, cube, w, out, st); break;
+    case 4: apply_launch_t<4>(pl, cube, w, out, st); break;
+    case 8: apply_launch_t<8>(pl, cube, w, out, st); break;
+    case 16: apply_launch_t<16>(pl, cube, w, out, st); break;
+    case 32: apply_launch_t<32>(pl, cube, w, out, st); break;
+  }
+}
+
+template <int SMAX>
+void apply_attr(size_t smem) {
+  cudaFuncSetAttribute(apply_kernel<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+void set_apply_attr(int smax, size_t smem) {
+  switch (smax) {
+    case 2: apply_attr<2>(smem); break;
+    case 4: apply_attr<4>(smem); break;
+    case 8: apply_attr<8>(smem); break;
+    case 16: apply_attr<16>(smem); break;
+    case 32: apply_attr<32>(smem); break;
+  }
+}
+
+stap_status check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libstap: launch failed: %s\n", cudaGetErrorString(e));
+    return STAP_ERR_CUDA;
+  }
+  return STAP_OK;
+}
+
+stap_status staged_run(const stap_plan* pl, const float2* cube, const float2* steer, float2* out,
+                       int32_t* info, void* ws, cudaStream_t st) {
+  char* w = static_cast<char*>(ws);
+  float2* cov = reinterpret_cast<float2*>(w);
+  float2* wts = reinterpret_cast<float2*>(w + pl->ws_cov);
+  float* gam = reinterpret_cast<float*>(w + pl->ws_cov + pl->ws_w);
+  cov_launch(pl, cube, cov, st);
+  solve_kernel<<<pl->solve_grid, pl->solve_wpc * 32, pl->solve_smem, st>>>(pl->kp.N, pl->kp.S, pl->units, cov,
+                                                                           steer, wts, gam, info);
+  apply_launch(pl, cube, wts, out, st);
+  return check_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t stap_abi_version(void) { return STAP_ABI_VERSION; }
+
+const char* stap_status_string(stap_status s) {
+  switch (s) {
+    case STAP_OK: return "STAP_OK";
+    case STAP_ERR_NULL_ARG: return "STAP_ERR_NULL_ARG: a required pointer is NULL";
+    case STAP_ERR_BAD_DIMS: return "STAP_ERR_BAD_DIMS: invalid dimensions, shard, cube window or workspace";
+    case STAP_ERR_UNSUPPORTED: return "STAP_ERR_UNSUPPORTED: valid but not implemented (N>64, S>32, C>8, odd K, window > smem)";
+    case STAP_ERR_MISALIGNED: return "STAP_ERR_MISALIGNED: device pointer not 16-byte aligned";
+    case STAP_ERR_CUDA: return "STAP_ERR_CUDA: CUDA runtime or launch error";
+    case STAP_ERR_DEVICE: return "STAP_ERR_DEVICE: no sm_100 device at the plan's ordinal";
+  }
+  return "STAP_ERR_UNKNOWN";
+}
+
+stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
+  if (!p || !out_plan) return STAP_ERR_NULL_ARG;
+  *out_plan = nullptr;
+  const int C = p->n_chan, T = p->tdof, D = p->n_dop, R = p->n_range, K = p->training_block,
+            S = p->n_steering;
+  if (C <= 0 || T <= 0 || D <= 0 || R <= 0 || K <= 0 || S <= 0 || p->batch <= 0) return STAP_ERR_BAD_DIMS;
+  if (R % K != 0 || T > D) return STAP_ERR_BAD_DIMS;
+  if (!(p->diag_load >= 0.0f) || !std::isfinite(p->diag_load)) return STAP_ERR_BAD_DIMS;
+  if (p->dop_begin < 0 || p->dop_count <= 0 || (long long)p->dop_begin + p->dop_count > D)
+    return STAP_ERR_BAD_DIMS;
+  if (p->cube_bins <= 0 || p->cube_bins > D || p->cube_bin0 < 0 || p->cube_bin0 >= D) return STAP_ERR_BAD_DIMS;
+  const int h = (T - 1) / 2;
+  if (p->cube_bins < D) {
+    long long off = ((long long)p->dop_begin - h - p->cube_bin0) % D;
+    if (off < 0) off += D;
+    if (off + p->dop_count + T - 1 > p->cube_bins) return STAP_ERR_BAD_DIMS;
+  }
+  const int N = C * T;
+  if (N > 64 || S > 32 || C > 8 || (K & 1) || K > 1024) return STAP_ERR_UNSUPPORTED;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || p->device < 0 || p->device >= ndev) {
+    cudaGetLastError();
+    return STAP_ERR_DEVICE;
+  }
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device) != cudaSuccess || major != 10)
+    return STAP_ERR_DEVICE;
+
+  stap_plan* pl = new (std::nothrow) stap_plan();
+  if (!pl) return STAP_ERR_CUDA;
+  pl->prm = *p;
+  KParams& kp = pl->kp;
+  kp.C = C; kp.T = T; kp.N = N; kp.D = D; kp.R = R; kp.K = K; kp.B = R / K; kp.S = S; kp.h = h;
+  kp.lam = p->diag_load;
+  kp.dop_begin = p->dop_begin; kp.dop_count = p->dop_count;
+  kp.bin0 = p->cube_bin0; kp.nbins = p->cube_bins; kp.batch = p->batch;
+  kp.cube_stride = (long long)p->cube_bins * C * R;
+  pl->units = (long long)p->batch * p->dop_count * kp.B;
+
+  // K1: bins per CTA -- the largest run with <= 128 threads and <= 100 KB of
+  // shared memory (two CTAs per SM), else the largest that fits at all.
+  int P = 0;
+  for (int q = 1; q <= p->dop_count && q <= 64; ++q) {
+    int thr = (cov_blocks(T, q + T - 1) + 31) / 32 * 32;
+    if (thr > 128 || cov_smem_bytes(C, T, K, q) > 100 * 1024) break;
+    P = q;
+  }
+  if (P == 0) {
+    int thr = (cov_blocks(T, T) + 31) / 32 * 32;
+    if (thr > 256 || cov_smem_bytes(C, T, K, 1) > kSmemCap) {
+      delete pl;
+      return STAP_ERR_UNSUPPORTED;
+    }
+    P = 1;
+  }
+  pl->cov_P = P;
+  pl->cov_threads = (cov_blocks(T, P + T - 1) + 31) / 32 * 32;
+  pl->cov_runs = (p->dop_count + P - 1) / P;
+  pl->cov_smem = cov_smem_bytes(C, T, K, P);
+
+  // K2: warps per CTA so that shared memory stays <= ~100 KB
+  size_t pw = solve_warp_smem_bytes(N, S);
+  int wpc = (int)((100 * 1024) / pw);
+  wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+  if (pw * wpc > kSmemCap) {
+    delete pl;
+    return STAP_ERR_UNSUPPORTED;
+  }
+  pl->solve_wpc = wpc;
+  pl->solve_smem = pw * wpc;
+  long long sg = (pl->units + wpc - 1) / wpc;
+  pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+
+  // K3
+  pl->apply_tpu = apply_tpu(K);
+  pl->apply_upc = 128 / pl->apply_tpu;
+  pl->apply_smax = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <= 16 ? 16 : 32;
+  pl->apply_smem = apply_smem_bytes(N, pl->apply_smax, pl->apply_upc);
+  pl->apply_grid = (int)((pl->units + pl->apply_upc - 1) / pl->apply_upc);
+
+  // K4: fused single-kernel path when it fits
+  pl->fused = fused_configure(kp, &pl->fcfg) ? 1 : 0;
+
+  // staged workspace
+  const long long NN = (long long)N * N;
+  pl->ws_cov = align_up((size_t)pl->units * NN * 8, 256);
+  pl->ws_w = align_up((size_t)pl->units * S * N * 8, 256);
+  pl->ws_g = align_up((size_t)pl->units * S * 4, 256);
+  pl->ws_total = pl->fused ? 0 : pl->ws_cov + pl->ws_w + pl->ws_g;
+  pl->cube_bytes = (size_t)p->batch * kp.cube_stride * 8;
+  pl->steer_bytes = (size_t)S * N * 8;
+  pl->out_bytes = (size_t)p->batch * p->dop_count * S * (size_t)R * 8;
+  pl->info_bytes = (size_t)pl->units * 4;
+
+  {
+    DeviceGuard g(p->device);
+    if (!g.ok) {
+      delete pl;
+      return STAP_ERR_DEVICE;
+    }
+    if (set_cov_attr(C, pl->cov_smem) != cudaSuccess) {
+      delete pl;
+      cudaGetLastError();
+      return STAP_ERR_CUDA;
+    }
+    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->solve_smem);
+    set_apply_attr(pl->apply_smax, pl->apply_smem);
+    if (pl->fused) fused_set_attr(pl->fcfg);
+    if (cudaGetLastError() != cudaSuccess) {
+      delete pl;
+      return STAP_ERR_CUDA;
+    }
+  }
+  if (pl->fused)
+    snprintf(pl->desc, sizeof pl->desc, "fused:%s", pl->fcfg.name);
+  else
+    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(wpc=%d)+apply(tpu=%d,upc=%d)",
+             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_wpc, pl->apply_tpu, pl->apply_upc);
+  *out_plan = pl;
+  return STAP_OK;
+}
+
+stap_status stap_plan_destroy(stap_plan* plan) {
+  delete plan;
+  return STAP_OK;
+}
+
+stap_status stap_plan_workspace_bytes(const stap_plan* pl, int32_t host_io, size_t* bytes) {
+  if (!pl || !bytes) return STAP_ERR_NULL_ARG;
+  size_t b = pl->ws_total;
+  if (host_io)
+    b += align_up(pl->cube_bytes, 256) + align_up(pl->steer_bytes, 256) + align_up(pl->out_bytes, 256) +
+         align_up(pl->info_bytes, 256);
+  *bytes = b;
+  return STAP_OK;
+}
+
+const char* stap_plan_describe(const stap_plan* pl) { return pl ? pl->desc : "(null plan)"; }
+
+stap_status stap_covariance(const stap_plan* pl, const stap_c64* cube, stap_c64* cov, cudaStream_t st) {
+  if (!pl || !cube || !cov) return STAP_ERR_NULL_ARG;
+  if (!aligned16(cube) || !aligned16(cov)) return STAP_ERR_MISALIGNED;
+  DeviceGuard g(pl->prm.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  cov_launch(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<float2*>(cov), st);
+  return check_launch();
+}
+
+stap_status stap_solve_weights(const stap_plan* pl, const stap_c64* cov, const stap_c64* steering,
+                               stap_c64* weights, float* gamma, int32_t* info, cudaStream_t st) {
+  if (!pl || !cov || !steering || !weights || !info) return STAP_ERR_NULL_ARG;
+  if (!aligned16(cov) || !aligned16(steering) || !aligned16(weights) || !aligned16(info) ||
+      (gamma && !aligned16(gamma)))
+    return STAP_ERR_MISALIGNED;
+  DeviceGuard g(pl->prm.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  solve_kernel<<<pl->solve_grid, pl->solve_wpc * 32, pl->solve_smem, st>>>(
+      pl->kp.N, pl->kp.S, pl->units, reinterpret_cast<const float2*>(cov),
+      reinterpret_cast<const float2*>(steering), reinterpret_cast<float2*>(weights), gamma, info);
+  return check_launch();
+}
+
+stap_status stap_apply(const stap_plan* pl, const stap_c64* cube, const stap_c64* weights, stap_c64* out,
+                       cudaStream_t st) {
+  if (!pl || !cube || !weights || !out) return STAP_ERR_NULL_ARG;
+  if (!aligned16(cube) || !aligned16(weights) || !aligned16(out)) return STAP_ERR_MISALIGNED;
+  DeviceGuard g(pl->prm.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  apply_launch(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<const float2*>(weights),
+               reinterpret_cast<float2*>(out), st);
+  return check_launch();
+}
+
+stap_status stap_run(const stap_plan* pl, const stap_c64* cube, const stap_c64* steering, stap_c64* out,
+                     int32_t* info, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  if (!pl || !cube || !steering || !out || !info) return STAP_ERR_NULL_ARG;
+  if (pl->ws_total && !workspace) return STAP_ERR_NULL_ARG;
+  if (workspace_bytes < pl->ws_total) return STAP_ERR_BAD_DIMS;
+  if (!aligned16(cube) || !aligned16(steering) || !aligned16(out) || !aligned16(info) ||
+      (workspace && !aligned16(workspace)))
+    return STAP_ERR_MISALIGNED;
+  DeviceGuard g(pl->prm.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  if (pl->fused) {
+    fused_launch(pl->fcfg, pl->kp, reinterpret_cast<const float2*>(cube), reinterpret_cast<const float2*>(steering),
+                 reinterpret_cast<float2*>(out), info, st);
+    return check_launch();
+  }
+  return staged_run(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<const float2*>(steering),
+                    reinterpret_cast<float2*>(out), info, workspace, st);
+}
+
+stap_status stap_run_host(const stap_plan* pl, const stap_c64* h_cube, const stap_c64* h_steering, stap_c64* h_out,
+                          int32_t* h_info, void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  if (!pl || !h_cube || !h_steering || !h_out || !h_info || !workspace) return STAP_ERR_NULL_ARG;
+  size_t need = 0;
+  stap_plan_workspace_bytes(pl, 1, &need);
+  if (workspace_bytes < need) return STAP_ERR_BAD_DIMS;
+  if (!aligned16(workspace)) return STAP_ERR_MISALIGNED;
+  DeviceGuard g(pl->prm.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  char* w = static_cast<char*>(workspace);
+  char* d_cube = w + pl->ws_total;
+  char* d_steer = d_cube + align_up(pl->cube_bytes, 256);
+  char* d_out = d_steer + align_up(pl->steer_bytes, 256);
+  char* d_info = d_out + align_up(pl->out_bytes, 256);
+  if (cudaMemcpyAsync(d_cube, h_cube, pl->cube_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(d_steer, h_steering, pl->steer_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return check_launch() == STAP_OK ? STAP_ERR_CUDA : STAP_ERR_CUDA;
+  stap_status s = stap_run(pl, reinterpret_cast<const stap_c64*>(d_cube), reinterpret_cast<const stap_c64*>(d_steer),
+                           reinterpret_cast<stap_c64*>(d_out), reinterpret_cast<int32_t*>(d_info), workspace,
+                           pl->ws_total, st);
+  if (s != STAP_OK) return s;
+  if (cudaMemcpyAsync(h_out, d_out, pl->out_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(h_info, d_info, pl->info_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+    cudaGetLastError();
+    return STAP_ERR_CUDA;
+  }
+  return STAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by
+element on identical seeded complex64 inputs (-m gpu).
+
+Tolerances:
+  Y per output vector (one (d, k) range line): rel-L2 <= 1e-3   (BASELINE.json north_star)
+  W per (unit, k): rel-L2 <= 1e-3; gamma: rel <= 1e-3
+  R per unit (Frobenius): rel <= 1e-5 (a K-term FP32 sum, no conditioning amplification)
+  apply on given weights: rel-L2 <= 1e-5 per output vector
+  info: bit-exact (both sides decide on pivot > 0 / finite; only clear-cut cases are tested)
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import OracleParams
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def stap(cuda_ok):
+    import __graft_entry__ as g
+    g.build_lib()
+    import paper_2203_06233_b200 as p
+    return p
+
+
+NT = max(1, (os.cpu_count() or 1))
+
+
+def OP(cfg, **kw):
+    return OracleParams(cfg.C, cfg.T, cfg.D, cfg.R, cfg.K, cfg.S, cfg.lam, **kw)
+
+
+def plan_for(stap, cfg, **kw):
+    return stap.StapPlan(stap.Dims(cfg.C, cfg.T, cfg.D, cfg.R, cfg.K, cfg.S, cfg.lam), device=0, **kw)
+
+
+def rel_lines(Yg, Yr):
+    """rel-L2 per output vector (last axis)."""
+    num = np.linalg.norm(Yg - Yr, axis=-1)
+    den = np.linalg.norm(Yr, axis=-1)
+    return num / np.maximum(den, 1e-30)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda(0)
+
+
+def run_gpu(stap, cfg, cube, st, staged=False, **kw):
+    plan = plan_for(stap, cfg, **kw)
+    dc = dev(cube).reshape(plan.cube_shape)
+    ds = dev(st)
+    if staged:
+        cov = plan.covariance(dc)
+        w, g, info = plan.solve_weights(cov, ds)
+        y = plan.apply(dc, w)
+        torch.cuda.synchronize()
+        return plan, y.cpu().numpy(), info.cpu().numpy(), cov.cpu().numpy(), w.cpu().numpy(), g.cpu().numpy()
+    y, info = plan.run(dc, ds)
+    torch.cuda.synchronize()
+    return plan, y.cpu().numpy(), info.cpu().numpy()
+
+
+# ---------------------------------------------------------------- whole path vs oracle
+@pytest.mark.parametrize("name", ["tiny", "small", "medium"])
+@pytest.mark.parametrize("staged", [False, True])
+def test_run_vs_oracle_full(stap, name, staged):
+    cfg = synth.CONFIGS[name]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula" if name != "tiny" else "random")
+    ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
+    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    Y, info = res[1][0], res[2][0]
+    err = rel_lines(Y, ref["Y"])
+    assert np.array_equal(info, ref["info"])
+    assert err.max() <= 1e-3, (name, staged, err.max(), res[0].description)
+
+
+@pytest.mark.parametrize("name", ["medium", "large"])
+def test_run_full_size_sampled(stap, name):
+    """Full BASELINE size on the GPU in the bench's launch configuration; the oracle
+    computes sampled Doppler bins one by one (edges + interior) from windowed buffers."""
+    cfg = synth.CONFIGS[name]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    plan, Y, info = run_gpu(stap, cfg, cube, st)
+    for d in (0, 1, cfg.D // 2, cfg.D - 1):
+        b0, nb = synth.shard_window(cfg, d, 1)
+        local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
+        ref = oracle.run(OP(cfg, dop_begin=d, dop_count=1, cube_bin0=b0, cube_bins=nb), local, st, nthreads=NT)
+        err = rel_lines(Y[0, d], ref["Y"][0])
+        assert np.array_equal(info[0, d], ref["info"][0])
+        assert err.max() <= 1e-3, (name, d, err.max(), plan.description)
+
+
+# ---------------------------------------------------------------- stages vs oracle
+@pytest.mark.parametrize("name", ["tiny", "small", "medium"])
+def test_covariance_vs_oracle(stap, name):
+    cfg = synth.CONFIGS[name]
+    cube = synth.datacube(cfg)
+    if name == "medium":
+        cfg2 = cfg
+        Rref, _ = oracle.covariance(OP(cfg2, dop_begin=0, dop_count=24), cube)
+    else:
+        Rref, _ = oracle.covariance(OP(cfg), cube)
+    plan = plan_for(stap, cfg)
+    cov = plan.covariance(dev(cube).reshape(plan.cube_shape)).cpu().numpy()[0]
+    cov = cov[:Rref.shape[0]]
+    num = np.linalg.norm((cov - Rref).reshape(cov.shape[0], cfg.B, -1), axis=-1)
+    den = np.linalg.norm(Rref.reshape(cov.shape[0], cfg.B, -1), axis=-1)
+    assert (num / den).max() <= 1e-5
+    # exact Hermitian mirror and real diagonal
+    assert np.array_equal(cov, np.conj(np.swapaxes(cov, -1, -2)))
+    assert np.all(np.diagonal(cov, axis1=-2, axis2=-1).imag == 0)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
+def test_solve_vs_oracle(stap, name):
+    """K2 fed the GPU's own complex64 covariance; the oracle solves the same bytes."""
+    cfg = synth.CONFIGS[name]
+    nd = min(cfg.D, 16)
+    sub = cfg.with_(D=max(nd, cfg.T))
+    cube = synth.datacube(sub)
+    st = synth.steering(sub, "random")
+    plan = plan_for(stap, sub)
+    dc = dev(cube).reshape(plan.cube_shape)
+    cov = plan.covariance(dc)
+    w, g, info = plan.solve_weights(cov, dev(st))
+    torch.cuda.synchronize()
+    cov_h = cov.cpu().numpy()
+    Wr, gr, ir = oracle.solve(cov_h, st)
+    assert np.array_equal(info.cpu().numpy(), ir)
+    e = rel_lines(w.cpu().numpy(), Wr)
+    assert e.max() <= 1e-3, e.max()
+    assert (np.abs(g.cpu().numpy() - gr) / gr).max() <= 1e-3
+    # distortionless response in FP32
+    W = w.cpu().numpy().astype(np.complex128)
+    resp = np.einsum("...kn,kn->...k", W.conj(), st.astype(np.complex128))
+    assert np.abs(resp - 1).max() <= 1e-4
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
+def test_apply_vs_oracle(stap, name):
+    cfg = synth.CONFIGS[name]
+    sub = cfg.with_(D=min(cfg.D, 8) if cfg.D > 8 else cfg.D)
+    cube = synth.datacube(sub)
+    rng = np.random.default_rng(1)
+    W = (rng.standard_normal((sub.D, sub.B, sub.S, sub.N)) + 1j * rng.standard_normal((sub.D, sub.B, sub.S, sub.N))
+         ).astype(np.complex64)
+    plan = plan_for(stap, sub)
+    y = plan.apply(dev(cube).reshape(plan.cube_shape), dev(W).reshape(plan.weights_shape)).cpu().numpy()[0]
+    Yr = oracle.apply(OP(sub), cube, W)
+    assert rel_lines(y, Yr).max() <= 1e-5
+
+
+# ---------------------------------------------------------------- closed forms through the GPU
+def test_E1_identity_covariance_gpu(stap):
+    """DFT-white cube: Rhat = I => w_k = s_k/||s_k||^2 and Y = s_k^H z / ||s_k||^2 (north_star pin)."""
+    cfg = synth.CONFIGS["small"]
+    cube = synth.cube_e1(cfg)
+    st = synth.steering(cfg, "random")
+    _, Y, info = run_gpu(stap, cfg, cube, st)
+    s = st.astype(np.complex128)
+    wexp = s / np.sum(np.abs(s) ** 2, axis=1, keepdims=True)
+    for d in (0, 7, cfg.D - 1):
+        Z = np.concatenate([cube[(d - cfg.h + t) % cfg.D] for t in range(cfg.T)], 0).astype(np.complex128)
+        assert rel_lines(Y[0, d], wexp.conj() @ Z).max() <= 1e-5
+    assert np.all(info == 0)
+
+
+def test_E3_target_gpu(stap):
+    cfg = synth.CONFIGS["small"]
+    cube = synth.datacube(cfg)
+    rng = np.random.default_rng(3)
+    st = (rng.integers(-3, 4, (cfg.S, cfg.N)) + 1j * rng.integers(-3, 4, (cfg.S, cfg.N))).astype(np.complex64)
+    st[:, 0] += 4
+    alpha = 3 - 2j
+    picks = [(0, 5, 1), (100, 77, 0), (cfg.D - 1, 511, 15)]
+    for d, r, k in picks:
+        for t in range(cfg.T):
+            cube[(d - cfg.h + t) % cfg.D, :, r] = alpha * st[k, t * cfg.C:(t + 1) * cfg.C]
+    _, Y, _ = run_gpu(stap, cfg, cube, st)
+    for d, r, k in picks:
+        assert abs(Y[0, d, k, r] - alpha) <= 1e-4 * abs(alpha)
+
+
+# ---------------------------------------------------------------- composition, shards, batch, determinism
+@pytest.mark.parametrize("name", ["small", "medium"])
+def test_fused_equals_staged(stap, name):
+    cfg = synth.CONFIGS[name]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    _, Yf, If = run_gpu(stap, cfg, cube, st)
+    res = run_gpu(stap, cfg, cube, st, staged=True)
+    assert np.array_equal(If, res[2])
+    assert rel_lines(Yf, res[1]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("name,G", [("tiny", 3), ("small", 2), ("small", 8), ("medium", 4)])
+def test_doppler_shards_bitwise(stap, name, G):
+    """P15: every shard plan on a slice+halo buffer reproduces the full run bitwise."""
+    cfg = synth.CONFIGS[name]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    _, Yfull, Ifull = run_gpu(stap, cfg, cube, st)
+    for g in range(G):
+        lo, cnt = synth.shard_range(cfg.D, G, g)
+        b0, nb = synth.shard_window(cfg, lo, cnt)
+        local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
+        _, Y, I = run_gpu(stap, cfg, local, st, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb)
+        assert np.array_equal(Y[0], Yfull[0, lo:lo + cnt])
+        assert np.array_equal(I[0], Ifull[0, lo:lo + cnt])
+
+
+def test_batch_bitwise(stap):
+    cfg = synth.CONFIGS["small"]
+    cubes = np.stack([synth.datacube(cfg, i) for i in range(3)])
+    st = synth.steering(cfg, "ula")
+    _, Yb, Ib = run_gpu(stap, cfg, cubes, st, batch=3)
+    for i in range(3):
+        _, Y1, I1 = run_gpu(stap, cfg, cubes[i], st)
+        assert np.array_equal(Yb[i], Y1[0]) and np.array_equal(Ib[i], I1[0])
+
+
+def test_determinism_and_immutability(stap):
+    cfg = synth.CONFIGS["small"]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    plan = plan_for(stap, cfg)
+    dc = dev(cube).reshape(plan.cube_shape)
+    ds = dev(st)
+    c0, s0 = dc.clone(), ds.clone()
+    y1, i1 = plan.run(dc, ds)
+    y2, i2 = plan.run(dc, ds)
+    plan.solve_weights(plan.covariance(dc), ds)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(i1, i2)
+    assert torch.equal(dc, c0) and torch.equal(ds, s0)
+
+
+def test_run_host_matches_device(stap):
+    cfg = synth.CONFIGS["small"]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    plan = plan_for(stap, cfg)
+    _, Yd, Id = run_gpu(stap, cfg, cube, st)
+    hc = torch.from_numpy(cube).pin_memory()
+    hs = torch.from_numpy(st).pin_memory()
+    ho = torch.empty(plan.out_shape, dtype=torch.complex64).pin_memory()
+    hi = torch.empty(plan.info_shape, dtype=torch.int32).pin_memory()
+    ws = torch.empty(plan.host_workspace_bytes, dtype=torch.uint8, device="cuda:0")
+    plan.run_host(hc, hs, ho, hi, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(ho.numpy(), Yd) and np.array_equal(hi.numpy(), Id)
+
+
+# ---------------------------------------------------------------- edge and degenerate cases
+@pytest.mark.parametrize("kw", [
+    dict(C=1, T=1, D=1, R=8, K=2, S=1),        # N = 1, D = T = 1
+    dict(C=8, T=8, D=8, R=64, K=32, S=32),     # maximum N = 64, S = 32
+    dict(C=3, T=5, D=5, R=24, K=6, S=3),       # D = T, odd C, odd S, K < N (loading keeps R PD)
+    dict(C=6, T=5, D=37, R=128, K=64, S=16),   # ragged bin runs
+    dict(C=5, T=2, D=11, R=40, K=4, S=7),      # C without a fused specialisation -> staged path
+    dict(C=2, T=4, D=9, R=32, K=16, S=5),      # even T (h = 1)
+])
+@pytest.mark.parametrize("staged", [False, True])
+def test_edge_shapes(stap, kw, staged):
+    cfg = synth.StapConfig("edge", lam=1e-2, cfg_id=7, **kw)
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "random")
+    ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
+    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    assert np.array_equal(res[2][0], ref["info"])
+    assert rel_lines(res[1][0], ref["Y"]).max() <= 1e-3
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_info_paths(stap, staged):
+    cfg = synth.CONFIGS["small"]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "random")
+    cube[:, :, cfg.K:2 * cfg.K] = 0          # block 1 zero everywhere -> info = 1
+    st[5] = 0                                 # steering 5 zero -> info = -6 elsewhere
+    ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
+    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    Y, info = res[1][0], res[2][0]
+    assert np.array_equal(info, ref["info"])
+    assert np.all(info[:, 1] == 1) and np.all(info[:, 0] == -6)
+    assert np.all(Y[:, :, cfg.K:2 * cfg.K] == 0) and np.all(Y[:, 5] == 0)
+    good = np.ones(Y.shape[:2], bool)
+    good[:, 5] = False
+    mask = np.ones(cfg.R, bool)
+    mask[cfg.K:2 * cfg.K] = False
+    assert rel_lines(Y[good][:, mask], ref["Y"][good][:, mask]).max() <= 1e-3
+
+
+def test_bad_pointer_alignment(stap):
+    cfg = synth.CONFIGS["tiny"]
+    plan = plan_for(stap, cfg)
+    buf = torch.zeros(plan.out_shape[1] * cfg.S * cfg.R * 2 + 8, dtype=torch.float32, device="cuda:0")
+    with pytest.raises(stap.StapError) as e:
+        stap.stap_covariance(plan.handle, buf.data_ptr() + 8, buf.data_ptr(), None)
+    assert e.value.code == 4
