@@ -6,137 +6,407 @@
 // info = j+1 and zeroes the unit's weights; a bad gamma_k sets info = -(k+1)
 // for the smallest such k and zeroes w_k.
 //
-// Design (v1): one warp per matrix, the matrix resident in shared memory.
-//  - Cholesky, left-looking by columns: lane owns rows i = lane, lane + 32; for
-//    column j every owned row i >= j forms x_i = R[i][j] - sum_{m<j} L[i][m] conj(L[j][m])
-//    (L[j][m] is a broadcast read), the pivot x_j is shuffled from its owner,
-//    then L[i][j] = x_i / sqrt(x_j).  Row stride N+1 complex keeps the per-lane
-//    row reads on distinct banks.
-//  - Solves: lane k owns right-hand side k (S <= 32); y / v live in shared
-//    memory [i][k] (row stride YS >= S, consecutive lanes on consecutive words),
-//    L is read by broadcast.
+// B200 design: one lane GROUP of PR x PC lanes per matrix (8 lanes for N <= 8
+// ... 64 lanes = 2 warps for N <= 64), the matrix REGISTER-resident in a 2-D
+// block-cyclic layout: element (i, l) of the lower triangle lives in lane
+// (i mod PR, l mod PC), register [i / PR][l / PC]; right-hand side element
+// (i, k) in lane (i mod PR, k mod PC), register [i / PR][k / PC].
+//   Cholesky + forward solve, right-looking: step j scales column j (its owners
+//   publish it in shared memory), finalises y_j (row-j owners publish it), and
+//   every lane applies the rank-1 update A[i][l] -= L[i][j] conj(L[l][j]) and
+//   B[i][k] -= L[i][j] y_j[k] to the elements it owns -- all independent FMAs.
+//   Back solve, row by row from the bottom: row i of L and v_i are published,
+//   every lane updates its rows above.
+// Register indices are compile-time (outer loops over register blocks are
+// unrolled, the inner position inside a block is a runtime loop), so nothing
+// spills to local memory.  Two group barriers per step; a failed pivot does not
+// break the loop (groups sharing a warp keep a uniform control flow).
 #pragma once
 #include "common.cuh"
 
 namespace stapk {
 
-__host__ __device__ inline int solve_ld(int N) { return N + 1; }
+template <int PR_, int PC_, int MR_, int MC_, int SC_>
+struct SolveCfg {
+  static constexpr int PR = PR_, PC = PC_, MR = MR_, MC = MC_, SC = SC_;
+  static constexpr int G = PR * PC;        // lanes per matrix
+  static constexpr int NMAX = (PR * MR < PC * MC) ? PR * MR : PC * MC;
+  static constexpr int SMAXC = PC * SC;    // right-hand sides per matrix (capacity)
+  // smallest register row-block u that can hold a lower-triangle element of register column-block v
+  __host__ __device__ static constexpr int umin(int v) { return (PC * v - PR + 1) <= 0 ? 0 : (PC * v - PR + 1 + PR - 1) / PR; }
+};
 
-// Warp-cooperative factor + solve.  On entry L[i*LD + l] (l <= i) holds the lower
-// triangle of R.  steer: [S][N] (shared or global).  On return Y[i*YS + k] holds
-// w_k[i] (0 for failed k / failed unit; columns S..YS-1 untouched) and, for
-// lane k < S, *gamma_lane = gamma_k (0 if failed).  Returns info (same on all lanes).
-__device__ __forceinline__ int warp_chol_solve(int N, int S, int YS, float2* L, float2* Y,
-                                               const float2* steer, float* gamma_lane) {
-  const int lane = threadIdx.x & 31;
-  const int LD = solve_ld(N);
+// Per-group shared scratch (floats / float2), sized for the config.
+template <class CF>
+struct SolveShared {
+  float2 col[CF::PR * CF::MR];   // column j of L (rows)
+  float2 row[CF::PC * CF::MC];   // row i of L (columns), back solve
+  float2 yb[CF::SMAXC];          // y_j (forward) / v_i (backward)
+  float rdiag[CF::PR * CF::MR];  // 1 / L[j][j]
+  float gpart[CF::PR][CF::SMAXC];
+  float gam[CF::SMAXC];
+  float xj;
+  int fail;
+};
+
+template <int G>
+__device__ __forceinline__ void group_sync(int bar_id) {
+  if constexpr (G <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(G) : "memory");
+  }
+}
+
+// Solve one matrix per group.  A must hold the lower triangle of R (entries with
+// row < N, col <= row; others are ignored), B the steering rows B[i][k] = s_k[i].
+// On return B holds w_k[i] (0 for failed k / failed unit) and the function
+// returns info (identical on all lanes of the group).  gam_out (lane-local,
+// per register column kv) receives gamma_k for the lane's k's.
+template <class CF>
+__device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR][CF::MC], float2 (&B)[CF::MR][CF::SC],
+                                                SolveShared<CF>& sh, int gl, int bar_id) {
+  constexpr int PR = CF::PR, PC = CF::PC, MR = CF::MR, MC = CF::MC, SC = CF::SC, G = CF::G;
+  const int p = gl / PC, q = gl - (gl / PC) * PC;
   int fail = 0;
-  for (int j = 0; j < N; ++j) {
-    float2 x0 = make_float2(0.f, 0.f), x1 = make_float2(0.f, 0.f);
-    const int i0 = lane, i1 = lane + 32;
-    if (i0 >= j && i0 < N) {
-      x0 = L[i0 * LD + j];
-      for (int m = 0; m < j; ++m) cmsub_conjb(x0, L[i0 * LD + m], L[j * LD + m]);
+
+  // ---------------- Cholesky + forward solve (right-looking)
+#pragma unroll
+  for (int v = 0; v < MC; ++v) {
+    for (int qq = 0; qq < PC; ++qq) {
+      const int j = PC * v + qq;
+      if (j >= N) break;  // uniform
+      const int pj = j % PR, uj = j / PR;
+      // (a) diag owner publishes the pivot
+      if (p == pj && q == qq) {
+        float x = 0.f;
+#pragma unroll
+        for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u)
+          if (u == uj) x = A[u][v].x;
+        sh.xj = x;
+      }
+      group_sync<G>(bar_id);
+      // (b) every lane: pivot, scale column j / finalise y_j
+      float x = sh.xj;
+      const bool ok = finite_pos(x);
+      if (!ok && !fail) fail = j + 1;
+      if (!ok) x = 1.0f;
+      const float d = sqrtf(x);
+      const float r = 1.0f / d;
+      if (gl == 0) sh.rdiag[j] = r;
+      if (q == qq) {
+#pragma unroll
+        for (int u = CF::umin(v); u < MR; ++u) {
+          const int i = PR * u + p;
+          if (i > j) {
+            A[u][v].x *= r;
+            A[u][v].y *= r;
+            sh.col[i] = A[u][v];
+          } else if (i == j) {
+            A[u][v] = make_float2(d, 0.f);
+          }
+        }
+      }
+      if (p == pj) {
+#pragma unroll
+        for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u) {
+          if (u == uj) {
+#pragma unroll
+            for (int kv = 0; kv < SC; ++kv) {
+              B[u][kv].x *= r;
+              B[u][kv].y *= r;
+              sh.yb[PC * kv + q] = B[u][kv];
+            }
+          }
+        }
+      }
+      group_sync<G>(bar_id);
+      // (c) rank-1 update of the trailing matrix and of the right-hand sides
+      float2 Li[MR], Ll[MC], yk[SC];
+#pragma unroll
+      for (int u = CF::umin(v); u < MR; ++u) Li[u] = sh.col[PR * u + p];
+#pragma unroll
+      for (int v2 = v; v2 < MC; ++v2) Ll[v2] = sh.col[PC * v2 + q];
+#pragma unroll
+      for (int kv = 0; kv < SC; ++kv) yk[kv] = sh.yb[PC * kv + q];
+#pragma unroll
+      for (int v2 = v; v2 < MC; ++v2) {
+        const int l = PC * v2 + q;
+#pragma unroll
+        for (int u = CF::umin(v2); u < MR; ++u) {
+          const int i = PR * u + p;
+          if (l > j && i >= l && i < N) cmsub_conjb(A[u][v2], Li[u], Ll[v2]);
+        }
+      }
+#pragma unroll
+      for (int u = CF::umin(v); u < MR; ++u) {
+        const int i = PR * u + p;
+        if (i > j && i < N) {
+#pragma unroll
+          for (int kv = 0; kv < SC; ++kv) cmsub(B[u][kv], Li[u], yk[kv]);
+        }
+      }
     }
-    if (i1 >= j && i1 < N) {
-      x1 = L[i1 * LD + j];
-      for (int m = 0; m < j; ++m) cmsub_conjb(x1, L[i1 * LD + m], L[j * LD + m]);
+  }
+
+  // ---------------- gamma_k = ||y_k||^2 (lane partials over its rows, then a fixed-order sum over p)
+  float gl_part[SC];
+#pragma unroll
+  for (int kv = 0; kv < SC; ++kv) {
+    float g = 0.f;
+#pragma unroll
+    for (int u = 0; u < MR; ++u) {
+      if (PR * u + p < N) {
+        g = fmaf(B[u][kv].x, B[u][kv].x, g);
+        g = fmaf(B[u][kv].y, B[u][kv].y, g);
+      }
     }
-    const float xj = __shfl_sync(0xffffffffu, j < 32 ? x0.x : x1.x, j & 31);
-    if (!finite_pos(xj)) {
-      fail = j + 1;
+    gl_part[kv] = g;
+    sh.gpart[p][PC * kv + q] = g;
+  }
+  group_sync<G>(bar_id);
+  if (p == 0) {
+#pragma unroll
+    for (int kv = 0; kv < SC; ++kv) {
+      float g = 0.f;
+#pragma unroll
+      for (int pp = 0; pp < PR; ++pp) g += sh.gpart[pp][PC * kv + q];
+      sh.gam[PC * kv + q] = g;
+    }
+  }
+  group_sync<G>(bar_id);
+  (void)gl_part;
+
+  // ---------------- back solve v = L^-H y (rows from the bottom)
+#pragma unroll
+  for (int ui = MR - 1; ui >= 0; --ui) {
+    for (int pi = PR - 1; pi >= 0; --pi) {
+      const int i = PR * ui + pi;
+      if (i >= N) continue;  // uniform
+      if (p == pi) {
+#pragma unroll
+        for (int v = 0; v < MC; ++v)
+          if (ui >= CF::umin(v)) sh.row[PC * v + q] = A[ui][v];
+        const float r = sh.rdiag[i];
+#pragma unroll
+        for (int kv = 0; kv < SC; ++kv) {
+          B[ui][kv].x *= r;
+          B[ui][kv].y *= r;
+          sh.yb[PC * kv + q] = B[ui][kv];
+        }
+      }
+      group_sync<G>(bar_id);
+      float2 vk[SC];
+#pragma unroll
+      for (int kv = 0; kv < SC; ++kv) vk[kv] = sh.yb[PC * kv + q];
+#pragma unroll
+      for (int u = 0; u <= ui; ++u) {
+        const int m = PR * u + p;
+        if (m < i) {
+          const float2 lim = sh.row[m];
+#pragma unroll
+          for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[u][kv], lim, vk[kv]);
+        }
+      }
+      group_sync<G>(bar_id);
+    }
+  }
+
+  // ---------------- normalise: w_k = v_k / gamma_k; zero failed k or a failed unit
+#pragma unroll
+  for (int kv = 0; kv < SC; ++kv) {
+    const int k = PC * kv + q;
+    const float g = sh.gam[k];
+    const bool gok = finite_pos(g) && !fail;
+    const float ig = gok ? 1.0f / g : 0.f;
+#pragma unroll
+    for (int u = 0; u < MR; ++u)
+      B[u][kv] = gok ? make_float2(B[u][kv].x * ig, B[u][kv].y * ig) : make_float2(0.f, 0.f);
+  }
+  if (fail) return fail;
+  // smallest failing k over the group (fixed-order scan of the published gammas)
+  int info = 0;
+  for (int k = 0; k < S; ++k)
+    if (!finite_pos(sh.gam[k])) {
+      info = -(k + 1);
       break;
     }
-    const float ljj = sqrtf(xj);
-    const float r = 1.0f / ljj;
-    __syncwarp();
-    if (i0 == j) L[j * LD + j] = make_float2(ljj, 0.f);
-    else if (i0 > j && i0 < N) L[i0 * LD + j] = make_float2(x0.x * r, x0.y * r);
-    if (i1 == j) L[j * LD + j] = make_float2(ljj, 0.f);
-    else if (i1 > j && i1 < N) L[i1 * LD + j] = make_float2(x1.x * r, x1.y * r);
-    __syncwarp();
-  }
-  const int k = lane;
-  const bool kact = k < S;
-  if (fail) {
-    for (int idx = lane; idx < N * YS; idx += 32) Y[idx] = make_float2(0.f, 0.f);
-    if (kact) *gamma_lane = 0.f;
-    __syncwarp();
-    return fail;
-  }
-  // forward: y_i = (s_i - sum_{m<i} L[i][m] y_m) / L[i][i]
-  float g = 0.f;
-  if (kact) {
-    for (int i = 0; i < N; ++i) {
-      float2 x = steer[k * N + i];
-      for (int m = 0; m < i; ++m) cmsub(x, L[i * LD + m], Y[m * YS + k]);
-      const float r = 1.0f / L[i * LD + i].x;
-      x.x *= r;
-      x.y *= r;
-      Y[i * YS + k] = x;
-      g = fmaf(x.x, x.x, g);
-      g = fmaf(x.y, x.y, g);
-    }
-  }
-  const bool gok = finite_pos(g);
-  if (kact) {
-    if (gok) {
-      // backward: v_i = (y_i - sum_{m>i} conj(L[m][i]) v_m) / L[i][i], in place
-      for (int i = N - 1; i >= 0; --i) {
-        float2 x = Y[i * YS + k];
-        for (int m = i + 1; m < N; ++m) cmsub_conja(x, L[m * LD + i], Y[m * YS + k]);
-        const float r = 1.0f / L[i * LD + i].x;
-        Y[i * YS + k] = make_float2(x.x * r, x.y * r);
-      }
-      const float ig = 1.0f / g;
-      for (int i = 0; i < N; ++i) {
-        const float2 v = Y[i * YS + k];
-        Y[i * YS + k] = make_float2(v.x * ig, v.y * ig);
-      }
-    } else {
-      for (int i = 0; i < N; ++i) Y[i * YS + k] = make_float2(0.f, 0.f);
-    }
-    *gamma_lane = gok ? g : 0.f;
-  }
-  const unsigned bad = __ballot_sync(0xffffffffu, kact && !gok);
-  __syncwarp();
-  return bad ? -(__ffs(bad)) : 0;
+  return info;
 }
 
-__host__ inline size_t solve_warp_smem_bytes(int N, int S) {
-  return ((size_t)N * solve_ld(N) + (size_t)N * S) * 8;
-}
-
-// `units` matrices back to back ([units][N][N]); weights [units][S][N]; gamma [units][S]; info [units].
-__global__ void __launch_bounds__(256) solve_kernel(int N, int S, long long units,
-                                                     const float2* __restrict__ cov,
-                                                     const float2* __restrict__ steer,
-                                                     float2* __restrict__ wout, float* __restrict__ gout,
-                                                     int32_t* __restrict__ info) {
+// Choose the group layout for N (grid PR x PC, register blocks MR x MC) and S (SC).
+// K2 kernel: `units` matrices [units][N][N] -> weights [units][S][N], gamma, info.
+template <class CF>
+__global__ void __launch_bounds__(256) solve_kernel(int N, int S, long long units, const float2* __restrict__ cov,
+                                                     const float2* __restrict__ steer, float2* __restrict__ wout,
+                                                     float* __restrict__ gout, int32_t* __restrict__ info) {
+  constexpr int G = CF::G, PR = CF::PR, PC = CF::PC, MR = CF::MR, MC = CF::MC, SC = CF::SC;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int LD = solve_ld(N);
-  float2* base = reinterpret_cast<float2*>(smem) + (size_t)warp * ((size_t)N * LD + (size_t)N * S);
-  float2* L = base;                   // [N][LD]
-  float2* Y = base + (size_t)N * LD;  // [N][S]
+  const int ngroups = blockDim.x / G;
+  const int grp = threadIdx.x / G, gl = threadIdx.x - grp * G;
+  SolveShared<CF>* shs = reinterpret_cast<SolveShared<CF>*>(smem);
+  SolveShared<CF>& sh = shs[grp];
+  float2* wst = reinterpret_cast<float2*>(smem + ngroups * sizeof(SolveShared<CF>)) + (size_t)grp * S * N;
+  const int p = gl / PC, q = gl - (gl / PC) * PC;
+  const int bar_id = 1 + grp;
+  // groups in one warp must run the same trip count: iterate over warp-uniform bases
+  constexpr int GPW = G < 32 ? 32 / G : 1;  // groups per warp
+  const int wgrp0 = (grp / GPW) * GPW;       // first group of this warp
+  const long long stride = (long long)gridDim.x * ngroups;
+  for (long long base = (long long)blockIdx.x * ngroups + wgrp0; base < units; base += stride) {
+    const long long uidx = base + (grp - wgrp0);
+    const bool valid = uidx < units;
+    const long long uu = valid ? uidx : units - 1;  // clamp: compute a duplicate, store nothing
+    const float2* Rg = cov + uu * N * N;
+    float2 A[MR][MC], B[MR][SC];
+#pragma unroll
+    for (int v = 0; v < MC; ++v)
+#pragma unroll
+      for (int u = CF::umin(v); u < MR; ++u) {
+        const int i = PR * u + p, l = PC * v + q;
+        A[u][v] = (i < N && l <= i) ? Rg[i * N + l] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+    for (int u = 0; u < MR; ++u)
+#pragma unroll
+      for (int kv = 0; kv < SC; ++kv) {
+        const int i = PR * u + p, k = PC * kv + q;
+        B[u][kv] = (i < N && k < S) ? steer[k * N + i] : make_float2(0.f, 0.f);
+      }
+    const int inf = group_chol_solve<CF>(N, S, A, B, sh, gl, bar_id);
+    // stage w [S][N] in shared memory, then coalesced store
+#pragma unroll
+    for (int u = 0; u < MR; ++u)
+#pragma unroll
+      for (int kv = 0; kv < SC; ++kv) {
+        const int i = PR * u + p, k = PC * kv + q;
+        if (i < N && k < S) wst[k * N + i] = B[u][kv];
+      }
+    group_sync<G>(bar_id);
+    if (valid) {
+      float2* Wg = wout + uu * S * N;
+      for (int idx = gl; idx < S * N; idx += G) Wg[idx] = wst[idx];
+      if (gout)
+        for (int k = gl; k < S; k += G) gout[uu * S + k] = (inf > 0) ? 0.f : (finite_pos(sh.gam[k]) ? sh.gam[k] : 0.f);
+      if (gl == 0) info[uu] = inf;
+    }
+    group_sync<G>(bar_id);
+  }
+}
 
-  for (long long u = (long long)blockIdx.x * nwarps + warp; u < units; u += (long long)gridDim.x * nwarps) {
-    const float2* Rg = cov + u * N * N;
-    for (int idx = lane; idx < N * N; idx += 32) {
-      const int i = idx / N, l = idx - i * N;
-      if (l <= i) L[i * LD + l] = Rg[idx];
-    }
-    __syncwarp();
-    float g = 0.f;
-    const int inf = warp_chol_solve(N, S, S, L, Y, steer, &g);
-    if (gout && lane < S) gout[u * S + lane] = g;
-    float2* Wg = wout + u * S * N;
-    for (int idx = lane; idx < S * N; idx += 32) {
-      const int kk = idx / N, i = idx - kk * N;
-      Wg[idx] = Y[i * S + kk];
-    }
-    if (lane == 0) info[u] = inf;
-    __syncwarp();
+
+// ---- host-side selection ---------------------------------------------------
+struct SolveSel {
+  int id;       // instantiation id
+  int G;        // lanes per matrix
+  size_t shared_bytes;  // per group: SolveShared
+};
+
+using SolveCfg0 = SolveCfg<2, 4, 4, 2, 1>;
+using SolveCfg1 = SolveCfg<2, 4, 4, 2, 2>;
+using SolveCfg2 = SolveCfg<2, 4, 4, 2, 4>;
+using SolveCfg3 = SolveCfg<2, 4, 4, 2, 8>;
+using SolveCfg4 = SolveCfg<4, 4, 3, 3, 1>;
+using SolveCfg5 = SolveCfg<4, 4, 3, 3, 2>;
+using SolveCfg6 = SolveCfg<4, 4, 3, 3, 4>;
+using SolveCfg7 = SolveCfg<4, 4, 3, 3, 8>;
+using SolveCfg8 = SolveCfg<4, 4, 4, 4, 1>;
+using SolveCfg9 = SolveCfg<4, 4, 4, 4, 2>;
+using SolveCfg10 = SolveCfg<4, 4, 4, 4, 4>;
+using SolveCfg11 = SolveCfg<4, 4, 4, 4, 8>;
+using SolveCfg12 = SolveCfg<4, 8, 6, 3, 1>;
+using SolveCfg13 = SolveCfg<4, 8, 6, 3, 2>;
+using SolveCfg14 = SolveCfg<4, 8, 6, 3, 4>;
+using SolveCfg15 = SolveCfg<4, 8, 8, 4, 1>;
+using SolveCfg16 = SolveCfg<4, 8, 8, 4, 2>;
+using SolveCfg17 = SolveCfg<4, 8, 8, 4, 4>;
+using SolveCfg18 = SolveCfg<8, 8, 6, 6, 1>;
+using SolveCfg19 = SolveCfg<8, 8, 6, 6, 2>;
+using SolveCfg20 = SolveCfg<8, 8, 6, 6, 4>;
+using SolveCfg21 = SolveCfg<8, 8, 7, 7, 1>;
+using SolveCfg22 = SolveCfg<8, 8, 7, 7, 2>;
+using SolveCfg23 = SolveCfg<8, 8, 7, 7, 4>;
+using SolveCfg24 = SolveCfg<8, 8, 8, 8, 1>;
+using SolveCfg25 = SolveCfg<8, 8, 8, 8, 2>;
+using SolveCfg26 = SolveCfg<8, 8, 8, 8, 4>;
+
+#define STAPK_SOLVE_CFGS(X) \
+  X(0, SolveCfg0) \
+  X(1, SolveCfg1) \
+  X(2, SolveCfg2) \
+  X(3, SolveCfg3) \
+  X(4, SolveCfg4) \
+  X(5, SolveCfg5) \
+  X(6, SolveCfg6) \
+  X(7, SolveCfg7) \
+  X(8, SolveCfg8) \
+  X(9, SolveCfg9) \
+  X(10, SolveCfg10) \
+  X(11, SolveCfg11) \
+  X(12, SolveCfg12) \
+  X(13, SolveCfg13) \
+  X(14, SolveCfg14) \
+  X(15, SolveCfg15) \
+  X(16, SolveCfg16) \
+  X(17, SolveCfg17) \
+  X(18, SolveCfg18) \
+  X(19, SolveCfg19) \
+  X(20, SolveCfg20) \
+  X(21, SolveCfg21) \
+  X(22, SolveCfg22) \
+  X(23, SolveCfg23) \
+  X(24, SolveCfg24) \
+  X(25, SolveCfg25) \
+  X(26, SolveCfg26)
+
+inline int sc_index(int S, int PC) {
+  const int sc = (S + PC - 1) / PC;
+  return sc <= 1 ? 0 : sc <= 2 ? 1 : sc <= 4 ? 2 : 3;
+}
+
+// false if (N, S) has no instantiation (N > 64 or S > capacity)
+inline bool solve_select(int N, int S, SolveSel* s) {
+  int id = -1;
+  if (N <= 8) id = 0 + sc_index(S, 4);
+  else if (N <= 12) id = 4 + sc_index(S, 4);
+  else if (N <= 16) id = 8 + sc_index(S, 4);
+  else if (N <= 24) id = (S <= 32) ? 12 + sc_index(S, 8) : -1;
+  else if (N <= 32) id = (S <= 32) ? 15 + sc_index(S, 8) : -1;
+  else if (N <= 48) id = 18 + sc_index(S, 8);
+  else if (N <= 56) id = 21 + sc_index(S, 8);
+  else if (N <= 64) id = 24 + sc_index(S, 8);
+  if (id < 0) return false;
+  if ((id >= 12) && sc_index(S, 8) > 2) return false;
+  switch (id) {
+#define X(I, CFT) \
+  case I: s->id = I; s->G = CFT::G; s->shared_bytes = sizeof(SolveShared<CFT>); break;
+    STAPK_SOLVE_CFGS(X)
+#undef X
+    default: return false;
+  }
+  return true;
+}
+
+inline size_t solve_smem_bytes(const SolveSel& s, int groups, int N, int S) {
+  return (size_t)groups * s.shared_bytes + (size_t)groups * S * N * 8;
+}
+
+inline void solve_set_attr(const SolveSel& s, size_t smem) {
+  switch (s.id) {
+#define X(I, CFT) \
+  case I: cudaFuncSetAttribute(solve_kernel<CFT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    STAPK_SOLVE_CFGS(X)
+#undef X
+  }
+}
+
+inline void solve_launch(const SolveSel& s, int grid, int threads, size_t smem, cudaStream_t st, int N, int S,
+                         long long units, const float2* cov, const float2* steer, float2* w, float* g, int32_t* info) {
+  switch (s.id) {
+#define X(I, CFT) \
+  case I: solve_kernel<CFT><<<grid, threads, smem, st>>>(N, S, units, cov, steer, w, g, info); break;
+    STAPK_SOLVE_CFGS(X)
+#undef X
   }
 }
 

@@ -25,7 +25,8 @@ struct stap_plan {
   int cov_P, cov_threads, cov_runs;
   size_t cov_smem;
   // K2
-  int solve_wpc, solve_grid;
+  SolveSel solve_sel;
+  int solve_groups, solve_grid;
   size_t solve_smem;
   // K3
   int apply_tpu, apply_upc, apply_smax, apply_grid;
@@ -149,8 +150,8 @@ stap_status staged_run(const stap_plan* pl, const float2* cube, const float2* st
   float2* wts = reinterpret_cast<float2*>(w + pl->ws_cov);
   float* gam = reinterpret_cast<float*>(w + pl->ws_cov + pl->ws_w);
   cov_launch(pl, cube, cov, st);
-  solve_kernel<<<pl->solve_grid, pl->solve_wpc * 32, pl->solve_smem, st>>>(pl->kp.N, pl->kp.S, pl->units, cov,
-                                                                           steer, wts, gam, info);
+  solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
+               pl->kp.S, pl->units, cov, steer, wts, gam, info);
   apply_launch(pl, cube, wts, out, st);
   return check_launch();
 }
@@ -235,18 +236,21 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   pl->cov_runs = (p->dop_count + P - 1) / P;
   pl->cov_smem = cov_smem_bytes(C, T, K, P);
 
-  // K2: warps per CTA so that shared memory stays <= ~100 KB
-  size_t pw = solve_warp_smem_bytes(N, S);
-  int wpc = (int)((100 * 1024) / pw);
-  wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
-  if (pw * wpc > kSmemCap) {
+  // K2: lane-group layout for (N, S); 256 threads per CTA
+  if (!solve_select(N, S, &pl->solve_sel)) {
     delete pl;
     return STAP_ERR_UNSUPPORTED;
   }
-  pl->solve_wpc = wpc;
-  pl->solve_smem = pw * wpc;
-  long long sg = (pl->units + wpc - 1) / wpc;
-  pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+  pl->solve_groups = 256 / pl->solve_sel.G;
+  pl->solve_smem = solve_smem_bytes(pl->solve_sel, pl->solve_groups, N, S);
+  if (pl->solve_smem > kSmemCap) {
+    delete pl;
+    return STAP_ERR_UNSUPPORTED;
+  }
+  {
+    long long sg = (pl->units + pl->solve_groups - 1) / pl->solve_groups;
+    pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+  }
 
   // K3
   pl->apply_tpu = apply_tpu(K);
@@ -280,7 +284,7 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
       cudaGetLastError();
       return STAP_ERR_CUDA;
     }
-    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->solve_smem);
+    solve_set_attr(pl->solve_sel, pl->solve_smem);
     set_apply_attr(pl->apply_smax, pl->apply_smem);
     if (pl->fused) fused_set_attr(pl->fcfg);
     if (cudaGetLastError() != cudaSuccess) {
@@ -291,8 +295,9 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   if (pl->fused)
     snprintf(pl->desc, sizeof pl->desc, "fused:%s", pl->fcfg.name);
   else
-    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(wpc=%d)+apply(tpu=%d,upc=%d)",
-             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_wpc, pl->apply_tpu, pl->apply_upc);
+    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(tpu=%d,upc=%d)",
+             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_sel.id, pl->solve_sel.G, pl->apply_tpu,
+             pl->apply_upc);
   *out_plan = pl;
   return STAP_OK;
 }
@@ -331,9 +336,9 @@ stap_status stap_solve_weights(const stap_plan* pl, const stap_c64* cov, const s
     return STAP_ERR_MISALIGNED;
   DeviceGuard g(pl->prm.device);
   if (!g.ok) return STAP_ERR_DEVICE;
-  solve_kernel<<<pl->solve_grid, pl->solve_wpc * 32, pl->solve_smem, st>>>(
-      pl->kp.N, pl->kp.S, pl->units, reinterpret_cast<const float2*>(cov),
-      reinterpret_cast<const float2*>(steering), reinterpret_cast<float2*>(weights), gamma, info);
+  solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
+               pl->kp.S, pl->units, reinterpret_cast<const float2*>(cov), reinterpret_cast<const float2*>(steering),
+               reinterpret_cast<float2*>(weights), gamma, info);
   return check_launch();
 }
 
