@@ -13,11 +13,14 @@
 // order no matter which CTA computes it, so the result is bitwise independent
 // of P, of the run alignment and of the Doppler shard.
 //
-// Staging: the window (W bins x C channels x K cells, each row K*8 contiguous
-// bytes in HBM) is copied to shared memory with 1-D bulk async copies (TMA
-// engine) completing on one mbarrier.  Shared layout [w][c][j] with a 16-byte
-// pad per bin, so lanes reading the same (c, j) of 8 consecutive bins hit 8
-// distinct 16-byte bank groups.  One thread owns one lag block: C x C complex
+// Staging: the window is streamed through shared memory in chunks of KC range
+// cells with 1-D bulk async copies (TMA engine, one copy per (bin, channel)
+// row, completing on an mbarrier), double-buffered so the copy of chunk c+2
+// overlaps the math on chunk c+1.  Tile layout [w][c][KC+2] plus 2 complex per
+// bin: the 16-byte row pad and bin pad put the rows two threads of a block and
+// four consecutive bins read on distinct 16-byte bank groups.  Two threads own
+// one lag block for even C >= 4 (TI = C/2 rows x C columns each, adjacent
+// lanes, so the column operand is a broadcast), one thread otherwise; complex
 // accumulators in registers, float4 (2 cells) loads along j.
 #pragma once
 #include "common.cuh"
@@ -25,31 +28,50 @@
 namespace stapk {
 
 __host__ __device__ inline int cov_blocks(int T, int W) { return T * W - T * (T - 1) / 2; }
-__host__ __device__ inline int cov_binstride(int C, int K) { return C * K + 2; }  // complex
-__host__ inline size_t cov_smem_bytes(int C, int T, int K, int P) {
-  const int W = P + T - 1;
-  size_t win = (size_t)W * cov_binstride(C, K) * 8;
-  size_t blk = (size_t)cov_blocks(T, W) * C * C * 8;
-  size_t body = win > blk ? win : blk;
-  body = (body + 15) & ~(size_t)15;
-  return body + 16 /*mbarrier*/ + (size_t)P * 4 /*delta*/ + 16;
+__host__ __device__ inline int cov_tpb(int C) { return (C >= 4 && (C & 1) == 0) ? 2 : 1; }  // threads per block
+__host__ __device__ inline int tile_rs(int KC) { return KC + 2; }                             // row stride (complex)
+__host__ __device__ inline int tile_bs(int C, int KC) { return C * (KC + 2) + 2; }            // bin stride (complex)
+// largest even divisor of K that is <= 32
+__host__ __device__ inline int cov_kc(int K) {
+  for (int kc = K < 32 ? K : 32; kc >= 2; kc -= 2)
+    if (K % kc == 0) return kc;
+  return 2;
 }
 
+struct CovLayout {
+  int KC, nchunks, nbuf;
+  size_t tile_bytes, body, total;
+};
+__host__ __device__ inline CovLayout cov_layout(int C, int T, int K, int P) {
+  CovLayout L;
+  L.KC = cov_kc(K);
+  L.nchunks = K / L.KC;
+  L.nbuf = L.nchunks > 1 ? 2 : 1;
+  L.tile_bytes = (((size_t)(P + T - 1) * tile_bs(C, L.KC) * 8) + 127) & ~(size_t)127;
+  size_t body = L.nbuf * L.tile_bytes;
+  const size_t blk = (size_t)cov_blocks(T, P + T - 1) * C * C * 8;
+  if (blk > body) body = blk;
+  L.body = (body + 127) & ~(size_t)127;
+  L.total = L.body + 16 /*2 mbarriers*/ + (size_t)P * 4 /*delta*/ + 16;
+  return L;
+}
+__host__ inline size_t cov_smem_bytes(int C, int T, int K, int P) { return cov_layout(C, T, K, P).total; }
 
-// Issue the bulk copies of a window of W bins (global bins d0-h .. d0-h+W-1,
-// wrapped) of training block b of cube n into xs[w*bstride + c*K + j]; one
-// mbarrier `bar` (initialised with count 1) completes when all bytes landed.
-// Called by warp 0 only.
-__device__ __forceinline__ void load_window(const KParams& p, const float2* __restrict__ cube, int n, int b,
-                                            int d0, int W, int C, int bstride, float2* xs, uint64_t* bar) {
-  const int lane = threadIdx.x & 31, K = p.K;
-  if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(W * C * K * 8));
+// Issue the bulk copies of cells [j0, j0+KC) of the W-bin window (global bins
+// d0-h .. d0-h+W-1, wrapped) of training block b of cube n into tile; the
+// mbarrier `bar` completes when all bytes have landed.  Warp-cooperative (one warp).
+__device__ __forceinline__ void load_window_chunk(const KParams& p, const float2* __restrict__ cube, int n, int b,
+                                                  int d0, int W, int C, int j0, int KC, float2* tile,
+                                                  uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const int rs = tile_rs(KC), bs = tile_bs(C, KC);
+  if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(W * C * KC * 8));
   __syncwarp();
-  const float2* cb = cube + (long long)n * p.cube_stride + (long long)b * K;
+  const float2* cb = cube + (long long)n * p.cube_stride + (long long)b * p.K + j0;
   for (int q = lane; q < W * C; q += 32) {
     const int w = q / C, c = q - w * C;
     const int lb = local_bin(p, d0 - p.h + w);
-    bulk_g2s(xs + w * bstride + c * K, cb + ((long long)lb * C + c) * p.R, (uint32_t)(K * 8), bar);
+    bulk_g2s(tile + w * bs + c * rs, cb + ((long long)lb * C + c) * p.R, (uint32_t)(KC * 8), bar);
   }
 }
 
@@ -64,25 +86,23 @@ __device__ __forceinline__ void lag_block_of(int t, int T, int W, int& w, int& l
 }
 __host__ __device__ inline int lag_block_index(int w, int l, int W) { return l * W - l * (l - 1) / 2 + w; }
 
-// acc[c][c2] = sum_j xa[c][j] conj(xb[c2][j]), j ascending (fixed order).
-template <int C>
-__device__ __forceinline__ void herk_block(const float2* xa, const float2* xb, int K, float2 (&acc)[C][C]) {
+// acc[u][c2] += sum_{j < KC} xa[u][j] conj(xb[c2][j]), j ascending (fixed order);
+// xa = TI rows (stride rs), xb = C rows (stride rs).
+template <int C, int TI>
+__device__ __forceinline__ void herk_chunk(const float2* xa, const float2* xb, int rs, int KC,
+                                           float2 (&acc)[TI][C]) {
+#pragma unroll(C >= 8 ? 1 : 2)
+  for (int j = 0; j < KC; j += 2) {
+    float4 a[TI];
 #pragma unroll
-  for (int c = 0; c < C; ++c)
-#pragma unroll
-    for (int c2 = 0; c2 < C; ++c2) acc[c][c2] = make_float2(0.f, 0.f);
-#pragma unroll 2
-  for (int j = 0; j < K; j += 2) {
-    float4 a[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) a[c] = *reinterpret_cast<const float4*>(xa + c * K + j);
+    for (int u = 0; u < TI; ++u) a[u] = *reinterpret_cast<const float4*>(xa + u * rs + j);
 #pragma unroll
     for (int c2 = 0; c2 < C; ++c2) {
-      const float4 bb = *reinterpret_cast<const float4*>(xb + c2 * K + j);
+      const float4 bb = *reinterpret_cast<const float4*>(xb + c2 * rs + j);
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        cmac_conj(acc[c][c2], make_float2(a[c].x, a[c].y), make_float2(bb.x, bb.y));
-        cmac_conj(acc[c][c2], make_float2(a[c].z, a[c].w), make_float2(bb.z, bb.w));
+      for (int u = 0; u < TI; ++u) {
+        cmac_conj(acc[u][c2], make_float2(a[u].x, a[u].y), make_float2(bb.x, bb.y));
+        cmac_conj(acc[u][c2], make_float2(a[u].z, a[u].w), make_float2(bb.z, bb.w));
       }
     }
   }
@@ -107,74 +127,118 @@ __device__ __forceinline__ float delta_from_blocks(const float2* blk, int C, int
   return lam * tr / (float)N;
 }
 
+// The lag-block HERK of one CTA over all K cells, streaming chunks through
+// `tiles` (nbuf buffers) with mbarriers bar[0..1]; on return (after a CTA
+// barrier) the scaled blocks are in blk[nblk][C][C] (which may alias tiles).
 template <int C>
-__global__ void __launch_bounds__(256) cov_kernel(KParams p, const float2* __restrict__ cube,
+__device__ __forceinline__ void cta_lag_blocks(const KParams& p, const float2* __restrict__ cube, int n, int b,
+                                               int d0, int W, const CovLayout& L, unsigned char* tiles,
+                                               uint64_t* bar, float2* blk) {
+  constexpr int TPB = (C >= 4 && (C & 1) == 0) ? 2 : 1;
+  constexpr int TI = C / TPB;
+  const int tid = threadIdx.x;
+  const int T = p.T;
+  const int nblk = cov_blocks(T, W);
+  const int KC = L.KC, rs = tile_rs(KC), bs = tile_bs(C, KC);
+  if (tid < 32) {
+    load_window_chunk(p, cube, n, b, d0, W, C, 0, KC, reinterpret_cast<float2*>(tiles), bar);
+    if (L.nchunks > 1)
+      load_window_chunk(p, cube, n, b, d0, W, C, KC, KC, reinterpret_cast<float2*>(tiles + L.tile_bytes), bar + 1);
+  }
+  const int bi = tid / TPB, hf = tid - bi * TPB;
+  int w, l;
+  lag_block_of(bi, T, W, w, l);
+  const bool active = bi < nblk;
+  float2 acc[TI][C];
+#pragma unroll
+  for (int u = 0; u < TI; ++u)
+#pragma unroll
+    for (int c2 = 0; c2 < C; ++c2) acc[u][c2] = make_float2(0.f, 0.f);
+  for (int ch = 0; ch < L.nchunks; ++ch) {
+    const int buf = ch & 1;
+    const float2* tile = reinterpret_cast<const float2*>(tiles + buf * L.tile_bytes);
+    mbar_wait(bar + buf, (ch >> 1) & 1);
+    if (active) herk_chunk<C, TI>(tile + w * bs + hf * TI * rs, tile + (w + l) * bs, rs, KC, acc);
+    __syncthreads();  // every thread is done with this buffer
+    if (ch + 2 < L.nchunks && tid < 32)
+      load_window_chunk(p, cube, n, b, d0, W, C, (ch + 2) * KC, KC,
+                        reinterpret_cast<float2*>(tiles + buf * L.tile_bytes), bar + buf);
+  }
+  const float invK = 1.0f / (float)p.K;
+  if (active) {
+#pragma unroll
+    for (int u = 0; u < TI; ++u)
+#pragma unroll
+      for (int c2 = 0; c2 < C; ++c2)
+        blk[(bi * C + hf * TI + u) * C + c2] = make_float2(acc[u][c2].x * invK, acc[u][c2].y * invK);
+  }
+  __syncthreads();
+}
+
+template <int C>
+__global__ void __launch_bounds__(256, ((C & 1) && C >= 5) ? 1 : 2) cov_kernel(KParams p, const float2* __restrict__ cube,
                                                    float2* __restrict__ cov, int P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int run = blockIdx.x, b = blockIdx.y, n = blockIdx.z;
-  const int T = p.T, K = p.K, N = p.N;
-  const int dl0 = run * P;                       // first owned (local) bin of this run
+  const int T = p.T, N = p.N;
+  const int dl0 = run * P;                  // first owned (local) bin of this run
   const int Prun = min(P, p.dop_count - dl0);
-  const int d0 = p.dop_begin + dl0;              // its global index
+  const int d0 = p.dop_begin + dl0;         // its global index
   const int W = Prun + T - 1;
-  const int nblk = cov_blocks(T, W);
-  const int bstride = cov_binstride(C, K);
-
-  float2* xs = reinterpret_cast<float2*>(smem);
-  const int Wmax = P + T - 1;
-  size_t body = (size_t)Wmax * bstride * 8;
-  size_t blkb = (size_t)cov_blocks(T, Wmax) * C * C * 8;
-  body = ((body > blkb ? body : blkb) + 15) & ~(size_t)15;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + body);
-  float* delta_s = reinterpret_cast<float*>(smem + body + 16);
+  const CovLayout L = cov_layout(C, T, p.K, P);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.body);
+  float* delta_s = reinterpret_cast<float*>(smem + L.body + 16);
+  float2* blk = reinterpret_cast<float2*>(smem);  // aliases the tiles after the HERK
 
   const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid < 32) load_window(p, cube, n, b, d0, W, C, bstride, xs, bar);
+  cta_lag_blocks<C>(p, cube, n, b, d0, W, L, smem, bar, blk);
 
-  int w, l;
-  lag_block_of(tid, T, W, w, l);
-  const bool active = tid < nblk;
-  float2 acc[C][C];
-  mbar_wait(bar, 0);
-  if (active) herk_block<C>(xs + w * bstride, xs + (w + l) * bstride, K, acc);
-  __syncthreads();  // window no longer read: reuse the space for the blocks
-
-  const float invK = 1.0f / (float)K;
-  float2* blk = reinterpret_cast<float2*>(smem);  // [nblk][C][C], already scaled by 1/K
-  if (active) {
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-#pragma unroll
-      for (int c2 = 0; c2 < C; ++c2)
-        blk[(tid * C + c) * C + c2] = make_float2(acc[c][c2].x * invK, acc[c][c2].y * invK);
-  }
-  __syncthreads();
-
-  // delta per bin of the run: lambda * tr(Rhat) / N, trace summed over i = t*C + c ascending.
-  // Lag-0 block of window bin w is block index w.
   if (tid < Prun) delta_s[tid] = delta_from_blocks(blk, C, T, N, p.lam, tid);
   __syncthreads();
 
-  // Assemble R_d for each bin of the run (both triangles; lower = conj of upper).
+  // Assemble R_d for each bin of the run (both triangles; lower = conj of upper):
+  // one warp per output row (bin pr, row i), lanes over column pairs (16-byte
+  // stores); a lane's column -> (t_l, c_l) split is computed once.
   const long long NN = (long long)N * N;
   float2* out = cov + (((long long)n * p.dop_count + dl0) * p.B + b) * NN;
   const long long ostride = (long long)p.B * NN;  // between consecutive bins
-  const int total = Prun * N * N;
-  for (int idx = tid; idx < total; idx += blockDim.x) {
-    const int pr = idx / (N * N);
-    const int rem = idx - pr * N * N;
-    const int i = rem / N, col = rem - i * N;
-    float2 v = rhat_from_blocks(blk, C, W, pr, i, col);
-    if (i == col) {
-      v.y = 0.f;
-      v.x += delta_s[pr];
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int colA = 2 * lane, colB = 2 * lane + 1;  // this lane's columns (N <= 64)
+  const int tA = colA / C, cA = colA - tA * C, tB = colB / C, cB = colB - tB * C;
+  const bool vec = (N & 1) == 0;
+  for (int row = warp; row < Prun * N; row += nwarps) {
+    const int pr = row / N, i = row - pr * N;
+    const int ti = i / C, ci = i - ti * C;
+    const float dl = delta_s[pr];
+    float2 v[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = e ? colB : colA, tl = e ? tB : tA, cl = e ? cB : cA;
+      float2 x = make_float2(0.f, 0.f);
+      if (col < N) {
+        if (ti < tl || (ti == tl && ci <= cl)) {
+          x = blk[(lag_block_index(pr + ti, tl - ti, W) * C + ci) * C + cl];
+        } else {
+          const float2 u = blk[(lag_block_index(pr + tl, ti - tl, W) * C + cl) * C + ci];
+          x = make_float2(u.x, -u.y);
+        }
+        if (col == i) x = make_float2(x.x + dl, 0.f);
+      }
+      v[e] = x;
     }
-    out[pr * ostride + rem] = v;
+    float2* orow = out + pr * ostride + (long long)i * N;
+    if (vec) {
+      if (colA < N) *reinterpret_cast<float4*>(orow + colA) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    } else {
+      if (colA < N) orow[colA] = v[0];
+      if (colB < N) orow[colB] = v[1];
+    }
   }
 }
 

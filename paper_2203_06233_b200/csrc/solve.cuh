@@ -129,19 +129,21 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       for (int v2 = v; v2 < MC; ++v2) Ll[v2] = sh.col[PC * v2 + q];
 #pragma unroll
       for (int kv = 0; kv < SC; ++kv) yk[kv] = sh.yb[PC * kv + q];
+      // Only lower-triangle entries right of column j must change; the others a
+      // lane holds (upper triangle, rows >= N) are never read as results, so
+      // they are updated unconditionally (no per-element predicate).
+      if (q > qq) {
 #pragma unroll
-      for (int v2 = v; v2 < MC; ++v2) {
-        const int l = PC * v2 + q;
+        for (int u = CF::umin(v); u < MR; ++u) cmsub_conjb(A[u][v], Li[u], Ll[v]);
+      }
 #pragma unroll
-        for (int u = CF::umin(v2); u < MR; ++u) {
-          const int i = PR * u + p;
-          if (l > j && i >= l && i < N) cmsub_conjb(A[u][v2], Li[u], Ll[v2]);
-        }
+      for (int v2 = v + 1; v2 < MC; ++v2) {
+#pragma unroll
+        for (int u = CF::umin(v2); u < MR; ++u) cmsub_conjb(A[u][v2], Li[u], Ll[v2]);
       }
 #pragma unroll
       for (int u = CF::umin(v); u < MR; ++u) {
-        const int i = PR * u + p;
-        if (i > j && i < N) {
+        if (PR * u + p > j) {  // finalised rows <= j keep y
 #pragma unroll
           for (int kv = 0; kv < SC; ++kv) cmsub(B[u][kv], Li[u], yk[kv]);
         }
@@ -200,13 +202,15 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
 #pragma unroll
       for (int kv = 0; kv < SC; ++kv) vk[kv] = sh.yb[PC * kv + q];
 #pragma unroll
-      for (int u = 0; u <= ui; ++u) {
-        const int m = PR * u + p;
-        if (m < i) {
-          const float2 lim = sh.row[m];
+      for (int u = 0; u < ui; ++u) {  // rows m = PR*u + p < i
+        const float2 lim = sh.row[PR * u + p];
 #pragma unroll
-          for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[u][kv], lim, vk[kv]);
-        }
+        for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[u][kv], lim, vk[kv]);
+      }
+      if (p < pi) {
+        const float2 lim = sh.row[PR * ui + p];
+#pragma unroll
+        for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[ui][kv], lim, vk[kv]);
       }
       group_sync<G>(bar_id);
     }
@@ -237,7 +241,7 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
 // Choose the group layout for N (grid PR x PC, register blocks MR x MC) and S (SC).
 // K2 kernel: `units` matrices [units][N][N] -> weights [units][S][N], gamma, info.
 template <class CF>
-__global__ void __launch_bounds__(256) solve_kernel(int N, int S, long long units, const float2* __restrict__ cov,
+__global__ void __launch_bounds__(256, (CF::SC >= 4 || CF::MR * CF::MC > 56) ? 1 : 2) solve_kernel(int N, int S, long long units, const float2* __restrict__ cov,
                                                      const float2* __restrict__ steer, float2* __restrict__ wout,
                                                      float* __restrict__ gout, int32_t* __restrict__ info) {
   constexpr int G = CF::G, PR = CF::PR, PC = CF::PC, MR = CF::MR, MC = CF::MC, SC = CF::SC;

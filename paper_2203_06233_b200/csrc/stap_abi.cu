@@ -14,6 +14,7 @@
 #include "cov.cuh"
 #include "fused.cuh"
 #include "solve.cuh"
+#include "solve_small.cuh"
 
 using namespace stapk;
 
@@ -26,6 +27,7 @@ struct stap_plan {
   size_t cov_smem;
   // K2
   SolveSel solve_sel;
+  int solve_small, solve_lanes;  // N <= 16: solve_small.cuh with `solve_lanes` lanes per matrix
   int solve_groups, solve_grid;
   size_t solve_smem;
   // K3
@@ -134,6 +136,16 @@ void set_apply_attr(int smax, size_t smem) {
   }
 }
 
+void solve_dispatch(const stap_plan* pl, const float2* cov, const float2* steer, float2* w, float* g, int32_t* info,
+                    cudaStream_t st) {
+  if (pl->solve_small)
+    solve_small_launch(pl->kp.N, pl->solve_lanes, pl->solve_grid, 256, pl->solve_smem, st, pl->kp.S, pl->units, cov,
+                       steer, w, g, info);
+  else
+    solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
+                 pl->kp.S, pl->units, cov, steer, w, g, info);
+}
+
 stap_status check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -150,8 +162,7 @@ stap_status staged_run(const stap_plan* pl, const float2* cube, const float2* st
   float2* wts = reinterpret_cast<float2*>(w + pl->ws_cov);
   float* gam = reinterpret_cast<float*>(w + pl->ws_cov + pl->ws_w);
   cov_launch(pl, cube, cov, st);
-  solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
-               pl->kp.S, pl->units, cov, steer, wts, gam, info);
+  solve_dispatch(pl, cov, steer, wts, gam, info, st);
   apply_launch(pl, cube, wts, out, st);
   return check_launch();
 }
@@ -215,16 +226,16 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   kp.cube_stride = (long long)p->cube_bins * C * R;
   pl->units = (long long)p->batch * p->dop_count * kp.B;
 
-  // K1: bins per CTA -- the largest run with <= 128 threads and <= 100 KB of
-  // shared memory (two CTAs per SM), else the largest that fits at all.
+  // K1: bins per CTA -- the largest run whose lag blocks fit 256 threads with
+  // <= 113 KB of shared memory (two CTAs per SM), else the largest that fits at all.
   int P = 0;
-  for (int q = 1; q <= p->dop_count && q <= 64; ++q) {
-    int thr = (cov_blocks(T, q + T - 1) + 31) / 32 * 32;
-    if (thr > 128 || cov_smem_bytes(C, T, K, q) > 100 * 1024) break;
+  for (int q = 1; q <= p->dop_count && q <= 128; ++q) {
+    int thr = (cov_tpb(C) * cov_blocks(T, q + T - 1) + 31) / 32 * 32;
+    if (thr > 256 || cov_smem_bytes(C, T, K, q) > 113 * 1024) break;
     P = q;
   }
   if (P == 0) {
-    int thr = (cov_blocks(T, T) + 31) / 32 * 32;
+    int thr = (cov_tpb(C) * cov_blocks(T, T) + 31) / 32 * 32;
     if (thr > 256 || cov_smem_bytes(C, T, K, 1) > kSmemCap) {
       delete pl;
       return STAP_ERR_UNSUPPORTED;
@@ -232,7 +243,7 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
     P = 1;
   }
   pl->cov_P = P;
-  pl->cov_threads = (cov_blocks(T, P + T - 1) + 31) / 32 * 32;
+  pl->cov_threads = (cov_tpb(C) * cov_blocks(T, P + T - 1) + 31) / 32 * 32;
   pl->cov_runs = (p->dop_count + P - 1) / P;
   pl->cov_smem = cov_smem_bytes(C, T, K, P);
 
@@ -249,6 +260,14 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   }
   {
     long long sg = (pl->units + pl->solve_groups - 1) / pl->solve_groups;
+    pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+  }
+  pl->solve_small = N <= 16;
+  if (pl->solve_small) {
+    pl->solve_lanes = S <= 16 ? 16 : 32;
+    const int per_cta = 8 * (32 / pl->solve_lanes);  // matrices per 256-thread CTA
+    pl->solve_smem = solve_small_smem(N, pl->solve_lanes, 256);
+    long long sg = (pl->units + per_cta - 1) / per_cta;
     pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
   }
 
@@ -284,7 +303,10 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
       cudaGetLastError();
       return STAP_ERR_CUDA;
     }
-    solve_set_attr(pl->solve_sel, pl->solve_smem);
+    if (pl->solve_small)
+      solve_small_set_attr(N, pl->solve_lanes, pl->solve_smem);
+    else
+      solve_set_attr(pl->solve_sel, pl->solve_smem);
     set_apply_attr(pl->apply_smax, pl->apply_smem);
     if (pl->fused) fused_set_attr(pl->fcfg);
     if (cudaGetLastError() != cudaSuccess) {
@@ -296,7 +318,8 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
     snprintf(pl->desc, sizeof pl->desc, "fused:%s", pl->fcfg.name);
   else
     snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(tpu=%d,upc=%d)",
-             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_sel.id, pl->solve_sel.G, pl->apply_tpu,
+             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
+             pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tpu,
              pl->apply_upc);
   *out_plan = pl;
   return STAP_OK;
@@ -336,9 +359,8 @@ stap_status stap_solve_weights(const stap_plan* pl, const stap_c64* cov, const s
     return STAP_ERR_MISALIGNED;
   DeviceGuard g(pl->prm.device);
   if (!g.ok) return STAP_ERR_DEVICE;
-  solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
-               pl->kp.S, pl->units, reinterpret_cast<const float2*>(cov), reinterpret_cast<const float2*>(steering),
-               reinterpret_cast<float2*>(weights), gamma, info);
+  solve_dispatch(pl, reinterpret_cast<const float2*>(cov), reinterpret_cast<const float2*>(steering),
+                 reinterpret_cast<float2*>(weights), gamma, info, st);
   return check_launch();
 }
 

@@ -1,0 +1,33 @@
+"""Summarise an ncu report: key metrics + top stall reasons per kernel (dev helper)."""
+import csv, subprocess, sys, io
+rep = sys.argv[1]
+pat = sys.argv[2] if len(sys.argv) > 2 else "."
+out = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{pat}", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr = rows[0]
+keys = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+        "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+        "smsp__inst_executed.sum", "smsp__thread_inst_executed_per_inst_executed.ratio"]
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    print("=====", d.get("Kernel Name", "")[:90])
+    for k in keys:
+        if k in d:
+            print(f"  {k:70s} {d[k]}")
+    st = []
+    for k, v in d.items():
+        if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio"):
+            try:
+                st.append((float(v.replace(",", "")), k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
+            except ValueError:
+                pass
+    st.sort(reverse=True)
+    print("  stalls/issue:", ", ".join(f"{n}={v:.2f}" for v, n in st[:8]))
