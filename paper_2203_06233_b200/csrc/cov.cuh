@@ -203,16 +203,24 @@ __global__ void __launch_bounds__(256, ((C & 1) && C >= 5) ? 1 : 2) cov_kernel(K
   __syncthreads();
 
   // Assemble R_d for each bin of the run (both triangles; lower = conj of upper):
-  // one warp per output row (bin pr, row i), lanes over column pairs (16-byte
-  // stores); a lane's column -> (t_l, c_l) split is computed once.
+  // a warp writes RPW = 32 / NP whole rows per iteration (NP = column pairs per
+  // row), one column pair per lane (16-byte stores); a lane's row slot and its
+  // columns' (t_l, c_l) split are computed once.
   const long long NN = (long long)N * N;
   float2* out = cov + (((long long)n * p.dop_count + dl0) * p.B + b) * NN;
   const long long ostride = (long long)p.B * NN;  // between consecutive bins
   const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int colA = 2 * lane, colB = 2 * lane + 1;  // this lane's columns (N <= 64)
+  const int NP = (N + 1) >> 1;
+  const int RPW = NP >= 32 ? 1 : 32 / NP;
+  const int slot = lane / NP, pair = lane - slot * NP;
+  const bool lane_on = slot < RPW && pair < NP;
+  const int colA = 2 * pair, colB = 2 * pair + 1;
   const int tA = colA / C, cA = colA - tA * C, tB = colB / C, cB = colB - tB * C;
   const bool vec = (N & 1) == 0;
-  for (int row = warp; row < Prun * N; row += nwarps) {
+  const int rows = Prun * N;
+  for (int row0 = warp * RPW; row0 < rows; row0 += nwarps * RPW) {
+    const int row = row0 + slot;
+    if (!lane_on || row >= rows) continue;
     const int pr = row / N, i = row - pr * N;
     const int ti = i / C, ci = i - ti * C;
     const float dl = delta_s[pr];
@@ -234,9 +242,9 @@ __global__ void __launch_bounds__(256, ((C & 1) && C >= 5) ? 1 : 2) cov_kernel(K
     }
     float2* orow = out + pr * ostride + (long long)i * N;
     if (vec) {
-      if (colA < N) *reinterpret_cast<float4*>(orow + colA) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+      *reinterpret_cast<float4*>(orow + colA) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
     } else {
-      if (colA < N) orow[colA] = v[0];
+      orow[colA] = v[0];
       if (colB < N) orow[colB] = v[1];
     }
   }

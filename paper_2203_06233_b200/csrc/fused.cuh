@@ -183,26 +183,36 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
       if (gl == 0) info[((long long)n * p.dop_count + dl) * p.B + b] = inf;
       float2* yb = out + (((long long)n * p.dop_count + dl) * S) * p.R + (long long)b * K;
       const float2* xw = xs + pr * bs;
-      for (int j = gl; j < K; j += G) {
-        float2 acc[SMAX];
+      // two range cells per lane per pass (j, j + G) share every weight load
+      for (int j = gl; j < K; j += 2 * G) {
+        const int j2 = j + G;
+        const bool two = j2 < K;
+        float2 acc0[SMAX], acc1[SMAX];
 #pragma unroll
-        for (int k = 0; k < SMAX; ++k) acc[k] = make_float2(0.f, 0.f);
+        for (int k = 0; k < SMAX; ++k) acc0[k] = acc1[k] = make_float2(0.f, 0.f);
         int i = 0;
         for (int t = 0; t < T; ++t) {
           for (int c = 0; c < C; ++c, ++i) {
-            const float2 z = xw[t * bs + c * rs + j];
+            const float2* zr = xw + t * bs + c * rs;
+            const float2 z0 = zr[j];
+            const float2 z1 = two ? zr[j2] : make_float2(0.f, 0.f);
             const float4* wv = reinterpret_cast<const float4*>(wsm + i * SMAX);
 #pragma unroll
             for (int k2 = 0; k2 < SMAX / 2; ++k2) {
               const float4 ww = wv[k2];
-              cmac_conja(acc[2 * k2], make_float2(ww.x, ww.y), z);
-              cmac_conja(acc[2 * k2 + 1], make_float2(ww.z, ww.w), z);
+              cmac_conja(acc0[2 * k2], make_float2(ww.x, ww.y), z0);
+              cmac_conja(acc1[2 * k2], make_float2(ww.x, ww.y), z1);
+              cmac_conja(acc0[2 * k2 + 1], make_float2(ww.z, ww.w), z0);
+              cmac_conja(acc1[2 * k2 + 1], make_float2(ww.z, ww.w), z1);
             }
           }
         }
 #pragma unroll
         for (int k = 0; k < SMAX; ++k)
-          if (k < S) yb[(long long)k * p.R + j] = acc[k];
+          if (k < S) {
+            yb[(long long)k * p.R + j] = acc0[k];
+            if (two) yb[(long long)k * p.R + j2] = acc1[k];
+          }
       }
     }
     group_sync<G>(bar_id);

@@ -81,15 +81,16 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
   // forward: y_i = (s_i - sum_{m<i} L[i][m] y_m) / L[i][i]; row i of L read as pairs
 #pragma unroll
   for (int i = 0; i < N; ++i) {
+    float2 e = make_float2(0.f, 0.f);  // odd-m partial sum: halves the dependent chain
 #pragma unroll
     for (int m = 0; m + 1 < i; m += 2) {
       const float4 l2 = *reinterpret_cast<const float4*>(&sh.L[i][m]);
       cmsub(Y[i], make_float2(l2.x, l2.y), Y[m]);
-      cmsub(Y[i], make_float2(l2.z, l2.w), Y[m + 1]);
+      cmsub(e, make_float2(l2.z, l2.w), Y[m + 1]);
     }
     if (i & 1) cmsub(Y[i], sh.L[i][i - 1], Y[i - 1]);
-    Y[i].x *= sh.rd[i];
-    Y[i].y *= sh.rd[i];
+    Y[i].x = (Y[i].x + e.x) * sh.rd[i];
+    Y[i].y = (Y[i].y + e.y) * sh.rd[i];
     asm volatile("" ::: "memory");  // keep each row's loads next to their use (register pressure)
   }
   float g = 0.f;
@@ -102,6 +103,7 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
     // v_i -= sum_{m>i} U[i][m] v_m, row i of U read as pairs
+    float2 e = make_float2(0.f, 0.f);
     if ((i + 1) & 1) {
       if (i + 1 < N) cmsub(Y[i], sh.U[i][i + 1], Y[i + 1]);
     }
@@ -109,13 +111,13 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
     for (int m = ((i + 2) & ~1); m + 1 < N; m += 2) {
       const float4 u2 = *reinterpret_cast<const float4*>(&sh.U[i][m]);
       cmsub(Y[i], make_float2(u2.x, u2.y), Y[m]);
-      cmsub(Y[i], make_float2(u2.z, u2.w), Y[m + 1]);
+      cmsub(e, make_float2(u2.z, u2.w), Y[m + 1]);
     }
     if ((N - ((i + 2) & ~1)) & 1) {
       if (N - 1 > i) cmsub(Y[i], sh.U[i][N - 1], Y[N - 1]);
     }
-    Y[i].x *= sh.rd[i];
-    Y[i].y *= sh.rd[i];
+    Y[i].x = (Y[i].x + e.x) * sh.rd[i];
+    Y[i].y = (Y[i].y + e.y) * sh.rd[i];
     asm volatile("" ::: "memory");
   }
   const bool kact = sl < S;
