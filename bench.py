@@ -386,6 +386,16 @@ def main():
                             extra={"kernel": "fused_kernel (stap_run)", "share_of_step": 1.0,
                                    "achieved_perbin_count": cnt_cfg["flops_fused_bin"] * M / t_launch / 1e12})
     roof["peak_source"] = pk["source"]
+    # measured DRAM traffic of this kernel/launch from the committed ncu --set full capture (profiles/)
+    tkey = f"{args.config}/{'staged-' + roof['kernel'] if staged else 'fused'}/{M}"
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(tkey)
+        if tr:
+            roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_source"] = f"profiles/{tr['report']}_ncu_summary.txt"
+    except Exception:
+        pass
 
     result = {
         "metric": "STAP datacubes/sec", "value": value, "unit": "cubes/s", "n_gpus": world, "steps": args.steps,

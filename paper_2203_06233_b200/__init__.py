@@ -18,7 +18,7 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstap.so")
+LIB_PATH = os.environ.get("STAP_LIB") or os.path.join(_HERE, "libstap.so")  # STAP_LIB: profiling builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

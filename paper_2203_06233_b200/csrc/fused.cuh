@@ -27,6 +27,17 @@
 
 namespace stapk {
 
+#ifdef STAPK_PROF
+// phase-cycle counters of the fused kernel (profiling builds only):
+// [0] lag-block HERK + delta (per CTA), [1] solves (per segment), [2] apply (per segment), [3] CTA total
+__device__ unsigned long long g_fused_prof[4];
+#define STAPK_PROF_T(v) const long long v = clock64()
+#define STAPK_PROF_ADD(i, x) atomicAdd(&g_fused_prof[i], (unsigned long long)(x))
+#else
+#define STAPK_PROF_T(v)
+#define STAPK_PROF_ADD(i, x)
+#endif
+
 struct FusedCfg {
   int C, SMAX, N, G, P, threads, runs;
   size_t smem;
@@ -150,6 +161,7 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
   float2* wsm = reinterpret_cast<float2*>(smem + lay.off_w) + (size_t)grp * N * SMAX;  // [N][SMAX]
   const int bar_id = 1 + grp;
 
+  STAPK_PROF_T(pt0);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -167,6 +179,8 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
   }
   if (tid < Prun) delta_s[tid] = delta_from_blocks(blk, C, T, N, p.lam, tid);
   __syncthreads();
+  STAPK_PROF_T(pt1);
+  if (tid == 0) STAPK_PROF_ADD(0, pt1 - pt0);
 
   // 4. bins round-robin over the solver segments (trip count uniform per warp)
   constexpr int GPW = G < 32 ? 32 / G : 1;
@@ -175,8 +189,11 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
     const int pr_raw = base + (grp - wg0);
     const bool valid = pr_raw < Prun;
     const int pr = valid ? pr_raw : Prun - 1;
+    STAPK_PROF_T(ps0);
     const int inf = SP::template solve_bin<C, SMAX>(p, blk, W, pr, delta_s[pr], steer, sh, gl, bar_id, wsm);
     group_sync<G>(bar_id);
+    STAPK_PROF_T(ps1);
+    if (gl == 0) STAPK_PROF_ADD(1, ps1 - ps0);
 
     const int dl = dl0 + pr;
     if (valid) {
@@ -216,7 +233,11 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
       }
     }
     group_sync<G>(bar_id);
+    STAPK_PROF_T(ps2);
+    if (gl == 0) STAPK_PROF_ADD(2, ps2 - ps1);
   }
+  STAPK_PROF_T(pt2);
+  if (tid == 0) STAPK_PROF_ADD(3, pt2 - pt0);
 }
 
 // ---- host-side selection / launch ------------------------------------------
@@ -247,6 +268,20 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
   STAPK_FUSED_CFGS(X)
 #undef X
   if (!G) return false;
+  // the kernel's real register count (for the occupancy estimate)
+  int regs = 128;
+  {
+    cudaFuncAttributes fa;
+    bool got = false;
+#define X(CC, SM, NN, SPT)                                                            \
+    if (!got && kp.C == CC && SMAX == SM && kp.N == NN)                                \
+      got = cudaFuncGetAttributes(&fa, fused_kernel<CC, SM, SPT>) == cudaSuccess;
+    STAPK_FUSED_CFGS(X)
+#undef X
+    if (got) regs = fa.numRegs;
+    cudaGetLastError();
+  }
+  const int regs_alloc = (regs + 7) & ~7;
   const size_t cap = 227 * 1024;
   int bestP = 0, bestT = 0;
   size_t bestS = 0;
@@ -258,11 +293,15 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
       if (cov_tpb(kp.C) * cov_blocks(kp.T, P + kp.T - 1) > threads) break;
       const FusedLayout L = fused_layout(kp.C, kp.T, kp.K, P, kp.N, SMAX, ng, shb);
       if (L.total > cap) break;
-      const int cta_per_sm = (int)((228 * 1024) / (L.total + 1024));
+      int cta_per_sm = (int)((228 * 1024) / (L.total + 1024));    // shared memory
+      const int by_regs = 65536 / (regs_alloc * threads);         // register file
+      if (by_regs < cta_per_sm) cta_per_sm = by_regs;
+      if (2048 / threads < cta_per_sm) cta_per_sm = 2048 / threads;
       if (cta_per_sm < 1) break;
       const int warps = cta_per_sm * threads / 32;
-      // prefer more resident warps, then less covariance work per bin (larger P)
-      const double score = (warps > 16 ? 16 : warps) * 1000.0 + P;
+      // prefer more resident warps and CTAs (independent phases overlap), then
+      // less covariance work per bin (larger P)
+      const double score = (warps > 32 ? 32 : warps) * 1000.0 + cta_per_sm * 100.0 + P;
       if (score > bestScore) {
         bestScore = score;
         bestP = P;
@@ -271,8 +310,10 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
       }
     }
   }
-  // the fused kernel only pays when the lag blocks keep most threads busy
-  if (bestP == 0 || cov_tpb(kp.C) * cov_blocks(kp.T, bestP + kp.T - 1) < bestT / 2) return false;
+  // the fused kernel only pays with enough resident warps to overlap its phases
+  // (>= 12 per SM) and when the lag blocks keep >= 1/3 of the threads busy
+  if (bestP == 0 || bestScore < 12000.0 || 3 * cov_tpb(kp.C) * cov_blocks(kp.T, bestP + kp.T - 1) < bestT)
+    return false;
   f->C = kp.C;
   f->SMAX = SMAX;
   f->N = kp.N;

@@ -91,8 +91,8 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       const bool ok = finite_pos(x);
       if (!ok && !fail) fail = j + 1;
       if (!ok) x = 1.0f;
-      const float d = sqrtf(x);
-      const float r = 1.0f / d;
+      const float r = rsqrtf(x);  // one MUFU on the pivot chain
+      const float d = x * r;
       if (gl == 0) sh.rdiag[j] = r;
       if (q == qq) {
 #pragma unroll

@@ -48,8 +48,8 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
     const bool ok = finite_pos(x);
     if (!ok && !fail) fail = j + 1;
     if (!ok) x = 1.0f;
-    const float d = sqrtf(x);
-    const float r = 1.0f / d;
+    const float r = rsqrtf(x);  // one MUFU on the pivot chain
+    const float d = x * r;
     if (sl == j) sh.rd[j] = r;
     if (sl > j) {
       A[j].x *= r;

@@ -423,4 +423,14 @@ stap_status stap_run_host(const stap_plan* pl, const stap_c64* h_cube, const sta
   return STAP_OK;
 }
 
+#ifdef STAPK_PROF
+// Profiling builds only: read and reset the fused kernel's phase-cycle counters.
+int stap_debug_fused_prof(unsigned long long* out4) {
+  cudaMemcpyFromSymbol(out4, g_fused_prof, sizeof(unsigned long long) * 4);
+  unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_fused_prof, z, sizeof z);
+  return (int)cudaGetLastError();
+}
+#endif
+
 }  // extern "C"
