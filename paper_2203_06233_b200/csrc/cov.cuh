@@ -59,16 +59,17 @@ __host__ inline size_t cov_smem_bytes(int C, int T, int K, int P) { return cov_l
 
 // Issue the bulk copies of cells [j0, j0+KC) of the W-bin window (global bins
 // d0-h .. d0-h+W-1, wrapped) of training block b of cube n into tile; the
-// mbarrier `bar` completes when all bytes have landed.  Warp-cooperative (one warp).
-__device__ __forceinline__ void load_window_chunk(const KParams& p, const float2* __restrict__ cube, int n, int b,
-                                                  int d0, int W, int C, int j0, int KC, float2* tile,
-                                                  uint64_t* bar) {
-  const int lane = threadIdx.x & 31;
+// mbarrier `bar` completes when all bytes have landed.  Every thread of the CTA
+// issues its share of the (bin, channel) row copies (one copy per thread for
+// typical windows), so the copies start together; one thread must have posted
+// the expected byte count on `bar` (window_chunk_bytes) before, behind a barrier.
+__host__ __device__ inline uint32_t window_chunk_bytes(int W, int C, int KC) { return (uint32_t)(W * C * KC * 8); }
+__device__ __forceinline__ void issue_window_chunk(const KParams& p, const float2* __restrict__ cube, int n, int b,
+                                                   int d0, int W, int C, int j0, int KC, float2* tile,
+                                                   uint64_t* bar) {
   const int rs = tile_rs(KC), bs = tile_bs(C, KC);
-  if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(W * C * KC * 8));
-  __syncwarp();
   const float2* cb = cube + (long long)n * p.cube_stride + (long long)b * p.K + j0;
-  for (int q = lane; q < W * C; q += 32) {
+  for (int q = threadIdx.x; q < W * C; q += blockDim.x) {
     const int w = q / C, c = q - w * C;
     const int lb = local_bin(p, d0 - p.h + w);
     bulk_g2s(tile + w * bs + c * rs, cb + ((long long)lb * C + c) * p.R, (uint32_t)(KC * 8), bar);
@@ -140,11 +141,15 @@ __device__ __forceinline__ void cta_lag_blocks(const KParams& p, const float2* _
   const int T = p.T;
   const int nblk = cov_blocks(T, W);
   const int KC = L.KC, rs = tile_rs(KC), bs = tile_bs(C, KC);
-  if (tid < 32) {
-    load_window_chunk(p, cube, n, b, d0, W, C, 0, KC, reinterpret_cast<float2*>(tiles), bar);
-    if (L.nchunks > 1)
-      load_window_chunk(p, cube, n, b, d0, W, C, KC, KC, reinterpret_cast<float2*>(tiles + L.tile_bytes), bar + 1);
+  const uint32_t cbytes = window_chunk_bytes(W, C, KC);
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, cbytes);
+    if (L.nchunks > 1) mbar_arrive_expect_tx(bar + 1, cbytes);
   }
+  __syncthreads();
+  issue_window_chunk(p, cube, n, b, d0, W, C, 0, KC, reinterpret_cast<float2*>(tiles), bar);
+  if (L.nchunks > 1)
+    issue_window_chunk(p, cube, n, b, d0, W, C, KC, KC, reinterpret_cast<float2*>(tiles + L.tile_bytes), bar + 1);
   const int bi = tid / TPB, hf = tid - bi * TPB;
   int w, l;
   lag_block_of(bi, T, W, w, l);
@@ -159,10 +164,11 @@ __device__ __forceinline__ void cta_lag_blocks(const KParams& p, const float2* _
     const float2* tile = reinterpret_cast<const float2*>(tiles + buf * L.tile_bytes);
     mbar_wait(bar + buf, (ch >> 1) & 1);
     if (active) herk_chunk<C, TI>(tile + w * bs + hf * TI * rs, tile + (w + l) * bs, rs, KC, acc);
+    if (tid == 0 && ch + 2 < L.nchunks) mbar_arrive_expect_tx(bar + buf, cbytes);  // next phase of this buffer
     __syncthreads();  // every thread is done with this buffer
-    if (ch + 2 < L.nchunks && tid < 32)
-      load_window_chunk(p, cube, n, b, d0, W, C, (ch + 2) * KC, KC,
-                        reinterpret_cast<float2*>(tiles + buf * L.tile_bytes), bar + buf);
+    if (ch + 2 < L.nchunks)
+      issue_window_chunk(p, cube, n, b, d0, W, C, (ch + 2) * KC, KC,
+                         reinterpret_cast<float2*>(tiles + buf * L.tile_bytes), bar + buf);
   }
   const float invK = 1.0f / (float)p.K;
   if (active) {
