@@ -28,6 +28,9 @@
 namespace stapk {
 
 __host__ __device__ inline int cov_blocks(int T, int W) { return T * W - T * (T - 1) / 2; }
+// staged lag-block stride (complex): C*C + 1 so the same element of consecutive blocks
+// falls on different banks (the HERK writes and the R assembly reads are conflict-free)
+__host__ __device__ inline int blk_stride(int C) { return C * C + 1; }
 __host__ __device__ inline int cov_tpb(int C) { return (C >= 4 && (C & 1) == 0) ? 2 : 1; }  // threads per block
 __host__ __device__ inline int tile_rs(int KC) { return KC + 2; }                             // row stride (complex)
 __host__ __device__ inline int tile_bs(int C, int KC) { return C * (KC + 2) + 2; }            // bin stride (complex)
@@ -49,7 +52,7 @@ __host__ __device__ inline CovLayout cov_layout(int C, int T, int K, int P) {
   L.nbuf = L.nchunks > 1 ? 2 : 1;
   L.tile_bytes = (((size_t)(P + T - 1) * tile_bs(C, L.KC) * 8) + 127) & ~(size_t)127;
   size_t body = L.nbuf * L.tile_bytes;
-  const size_t blk = (size_t)cov_blocks(T, P + T - 1) * C * C * 8;
+  const size_t blk = (size_t)cov_blocks(T, P + T - 1) * blk_stride(C) * 8;
   if (blk > body) body = blk;
   L.body = (body + 127) & ~(size_t)127;
   L.total = L.body + 16 /*2 mbarriers*/ + (size_t)P * 4 /*delta*/ + 16;
@@ -114,9 +117,9 @@ __device__ __forceinline__ void herk_chunk(const float2* xa, const float2* xb, i
 __device__ __forceinline__ float2 rhat_from_blocks(const float2* blk, int C, int W, int pr, int i, int col) {
   const int ti = i / C, ci = i - ti * C, tl = col / C, cl = col - tl * C;
   if (ti < tl || (ti == tl && ci <= cl)) {
-    return blk[(lag_block_index(pr + ti, tl - ti, W) * C + ci) * C + cl];
+    return blk[lag_block_index(pr + ti, tl - ti, W) * blk_stride(C) + ci * C + cl];
   }
-  const float2 u = blk[(lag_block_index(pr + tl, ti - tl, W) * C + cl) * C + ci];
+  const float2 u = blk[lag_block_index(pr + tl, ti - tl, W) * blk_stride(C) + cl * C + ci];
   return make_float2(u.x, -u.y);
 }
 
@@ -124,7 +127,7 @@ __device__ __forceinline__ float2 rhat_from_blocks(const float2* blk, int C, int
 __device__ __forceinline__ float delta_from_blocks(const float2* blk, int C, int T, int N, float lam, int pr) {
   float tr = 0.f;
   for (int t = 0; t < T; ++t)
-    for (int c = 0; c < C; ++c) tr += blk[((pr + t) * C + c) * C + c].x;
+    for (int c = 0; c < C; ++c) tr += blk[(pr + t) * blk_stride(C) + c * C + c].x;
   return lam * tr / (float)N;
 }
 
@@ -176,7 +179,7 @@ __device__ __forceinline__ void cta_lag_blocks(const KParams& p, const float2* _
     for (int u = 0; u < TI; ++u)
 #pragma unroll
       for (int c2 = 0; c2 < C; ++c2)
-        blk[(bi * C + hf * TI + u) * C + c2] = make_float2(acc[u][c2].x * invK, acc[u][c2].y * invK);
+        blk[bi * blk_stride(C) + (hf * TI + u) * C + c2] = make_float2(acc[u][c2].x * invK, acc[u][c2].y * invK);
   }
   __syncthreads();
 }
@@ -237,9 +240,9 @@ __global__ void __launch_bounds__(256, ((C & 1) && C >= 5) ? 1 : 2) cov_kernel(K
       float2 x = make_float2(0.f, 0.f);
       if (col < N) {
         if (ti < tl || (ti == tl && ci <= cl)) {
-          x = blk[(lag_block_index(pr + ti, tl - ti, W) * C + ci) * C + cl];
+          x = blk[lag_block_index(pr + ti, tl - ti, W) * blk_stride(C) + ci * C + cl];
         } else {
-          const float2 u = blk[(lag_block_index(pr + tl, ti - tl, W) * C + cl) * C + ci];
+          const float2 u = blk[lag_block_index(pr + tl, ti - tl, W) * blk_stride(C) + cl * C + ci];
           x = make_float2(u.x, -u.y);
         }
         if (col == i) x = make_float2(x.x + dl, 0.f);

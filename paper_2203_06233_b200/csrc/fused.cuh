@@ -53,7 +53,7 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int T, int K, int P, 
   FusedLayout L;
   size_t o = (((size_t)(P + T - 1) * tile_bs(C, K) * 8) + 127) & ~(size_t)127;  // whole window, KC = K
   L.off_blk = o;
-  o += (((size_t)cov_blocks(T, P + T - 1) * C * C * 8) + 127) & ~(size_t)127;
+  o += (((size_t)cov_blocks(T, P + T - 1) * blk_stride(C) * 8) + 127) & ~(size_t)127;
   L.off_sh = o;
   o += ((ngroups * sh_bytes) + 127) & ~(size_t)127;
   L.off_w = o;

@@ -22,6 +22,8 @@
 // spills to local memory.  Two group barriers per step; a failed pivot does not
 // break the loop (groups sharing a warp keep a uniform control flow).
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace stapk {
@@ -381,6 +383,10 @@ inline bool solve_select(int N, int S, SolveSel* s) {
   else if (N <= 64) id = 24 + sc_index(S, 8);
   if (id < 0) return false;
   if ((id >= 12) && sc_index(S, 8) > 2) return false;
+  if (const char* e = getenv("STAP_SOLVE_ID")) {  // developer A/B knob: force a compatible layout
+    const int f = atoi(e);
+    if (f >= 0 && f <= 26) id = f;
+  }
   switch (id) {
 #define X(I, CFT) \
   case I: s->id = I; s->G = CFT::G; s->shared_bytes = sizeof(SolveShared<CFT>); break;
