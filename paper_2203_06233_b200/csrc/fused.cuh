@@ -67,6 +67,9 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int T, int K, int P, 
 template <class CF>
 struct GroupSolverPolicy {
   static constexpr int G = CF::G;
+  static constexpr int kMaxThreads = 256, kMinBlocks = CF::G > 32 ? 1 : 2;
+  static constexpr bool kWInShared = false;
+  static constexpr int kN = 0;
   using Shared = SolveShared<CF>;
   template <int C, int SMAX>
   __device__ static __forceinline__ int solve_bin(const KParams& p, const float2* blk, int W, int pr, float dlt,
@@ -110,6 +113,9 @@ struct GroupSolverPolicy {
 template <int NN, int LANES>
 struct SmallSolverPolicy {
   static constexpr int G = LANES;
+  static constexpr int kMaxThreads = 128, kMinBlocks = 5;  // registers <= 102: 5 CTAs (20 warps) per SM
+  static constexpr bool kWInShared = true;                 // w_k aliases the L/U scratch after the solve
+  static constexpr int kN = NN;
   using Shared = SmallShared<NN>;
   template <int C, int SMAX>
   __device__ static __forceinline__ int solve_bin(const KParams& p, const float2* blk, int W, int pr, float dlt,
@@ -135,10 +141,11 @@ struct SmallSolverPolicy {
 };
 
 template <int C, int SMAX, class SP>
-__global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams p, const float2* __restrict__ cube,
-                                                     const float2* __restrict__ steer, float2* __restrict__ out,
-                                                     int32_t* __restrict__ info, int P) {
+__global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
+    fused_kernel(KParams p, const float2* __restrict__ cube, const float2* __restrict__ steer,
+                 float2* __restrict__ out, int32_t* __restrict__ info, int P) {
   constexpr int G = SP::G;
+  static_assert(!SP::kWInShared || sizeof(typename SP::Shared) >= (size_t)SP::kN * SMAX * 8, "w alias too small");
   extern __shared__ __align__(128) unsigned char smem[];
   const int run = blockIdx.x, b = blockIdx.y, n = blockIdx.z;
   const int T = p.T, K = p.K, N = p.N, S = p.S;
@@ -147,7 +154,8 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
   const int Prun = min(P, p.dop_count - dl0);
   const int d0 = p.dop_begin + dl0;
   const int W = Prun + T - 1;
-  const FusedLayout lay = fused_layout(C, T, K, P, N, SMAX, ngroups, sizeof(typename SP::Shared));
+  const FusedLayout lay = fused_layout(C, T, K, P, SP::kWInShared ? 0 : N, SMAX, ngroups,
+                                       sizeof(typename SP::Shared));
 
   float2* xs = reinterpret_cast<float2*>(smem);
   float2* blk = reinterpret_cast<float2*>(smem + lay.off_blk);
@@ -158,7 +166,9 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
   const int tid = threadIdx.x;
   const int grp = tid / G, gl = tid - grp * G;
   typename SP::Shared& sh = reinterpret_cast<typename SP::Shared*>(smem + lay.off_sh)[grp];
-  float2* wsm = reinterpret_cast<float2*>(smem + lay.off_w) + (size_t)grp * N * SMAX;  // [N][SMAX]
+  // w_k as [N][SMAX]: its own region, or aliased onto this segment's solver scratch
+  float2* wsm = SP::kWInShared ? reinterpret_cast<float2*>(&sh)
+                               : reinterpret_cast<float2*>(smem + lay.off_w) + (size_t)grp * N * SMAX;
   const int bar_id = 1 + grp;
 
   STAPK_PROF_T(pt0);
@@ -190,13 +200,22 @@ __global__ void __launch_bounds__(256, SP::G > 32 ? 1 : 2) fused_kernel(KParams 
     const bool valid = pr_raw < Prun;
     const int pr = valid ? pr_raw : Prun - 1;
     STAPK_PROF_T(ps0);
+#if defined(STAPK_SKIP) && STAPK_SKIP >= 2  // dev builds only: phase-cost experiments
+    const int inf = 0;
+#else
     const int inf = SP::template solve_bin<C, SMAX>(p, blk, W, pr, delta_s[pr], steer, sh, gl, bar_id, wsm);
+#endif
     group_sync<G>(bar_id);
     STAPK_PROF_T(ps1);
     if (gl == 0) STAPK_PROF_ADD(1, ps1 - ps0);
 
     const int dl = dl0 + pr;
+#if defined(STAPK_SKIP) && STAPK_SKIP >= 1
+    if (valid && gl == 0) info[((long long)n * p.dop_count + dl) * p.B + b] = inf;
+    if (false) {
+#else
     if (valid) {
+#endif
       if (gl == 0) info[((long long)n * p.dop_count + dl) * p.B + b] = inf;
       float2* yb = out + (((long long)n * p.dop_count + dl) * S) * p.R + (long long)b * K;
       const float2* xw = xs + pr * bs;
@@ -258,11 +277,13 @@ inline int fused_smax(int S) { return S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <
 inline bool fused_configure(const KParams& kp, FusedCfg* f) {
   memset(f, 0, sizeof *f);
   const int SMAX = fused_smax(kp.S);
-  int G = 0;
+  int G = 0, maxT = 0, wN = 0;
   size_t shb = 0;
 #define X(CC, SM, NN, SPT)                                       \
   if (kp.C == CC && SMAX == SM && kp.N == NN && kp.S <= 16) {    \
     G = SPT::G;                                                  \
+    maxT = SPT::kMaxThreads;                                     \
+    wN = SPT::kWInShared ? 0 : NN;                               \
     shb = sizeof(typename SPT::Shared);                          \
   }
   STAPK_FUSED_CFGS(X)
@@ -286,12 +307,12 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
   int bestP = 0, bestT = 0;
   size_t bestS = 0;
   double bestScore = -1.0;
-  for (int threads = 128; threads <= 256; threads += 128) {
+  for (int threads = 128; threads <= maxT; threads += 128) {
     if (threads % G) continue;
     const int ng = threads / G;
     for (int P = 1; P <= kp.dop_count && P <= 64; ++P) {
       if (cov_tpb(kp.C) * cov_blocks(kp.T, P + kp.T - 1) > threads) break;
-      const FusedLayout L = fused_layout(kp.C, kp.T, kp.K, P, kp.N, SMAX, ng, shb);
+      const FusedLayout L = fused_layout(kp.C, kp.T, kp.K, P, wN, SMAX, ng, shb);
       if (L.total > cap) break;
       int cta_per_sm = (int)((228 * 1024) / (L.total + 1024));    // shared memory
       const int by_regs = 65536 / (regs_alloc * threads);         // register file

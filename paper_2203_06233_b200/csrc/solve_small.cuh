@@ -42,21 +42,19 @@ template <int N, int LANES>
 __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const float2* __restrict__ steer,
                                                 float2 (&Y)[N], SmallShared<N>& sh, int sl, float* gamma) {
   int fail = 0;
+  // Branch-free steps (selects, not if/else): the segment shuffles then sit in
+  // provably convergent code and compile to bare SHFLs (no convergence loops).
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     float x = __shfl_sync(0xffffffffu, A[j].x, j, LANES);
     const bool ok = finite_pos(x);
-    if (!ok && !fail) fail = j + 1;
-    if (!ok) x = 1.0f;
+    fail = (!ok && !fail) ? j + 1 : fail;
+    x = ok ? x : 1.0f;
     const float r = rsqrtf(x);  // one MUFU on the pivot chain
     const float d = x * r;
     if (sl == j) sh.rd[j] = r;
-    if (sl > j) {
-      A[j].x *= r;
-      A[j].y *= r;
-    } else if (sl == j) {
-      A[j] = make_float2(d, 0.f);
-    }
+    const float2 a = A[j];
+    A[j] = sl > j ? make_float2(a.x * r, a.y * r) : (sl == j ? make_float2(d, 0.f) : a);
 #pragma unroll
     for (int l = j + 1; l < N; ++l) {
       const float2 Llj = seg_shfl<N, LANES>(A[j], l);

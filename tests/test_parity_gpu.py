@@ -307,3 +307,43 @@ def test_bad_pointer_alignment(stap):
     with pytest.raises(stap.StapError) as e:
         stap.stap_covariance(plan.handle, buf.data_ptr() + 8, buf.data_ptr(), None)
     assert e.value.code == 4
+
+
+# ---------------------------------------------------------------- race / stability stress (compute-sanitizer is closed on this pool)
+@pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
+def test_repeat_runs_bitwise(stap, name):
+    """Shared-memory races (mbarrier phases, aliased scratch, group barriers) show up as
+    run-to-run differences: 8 repeated launches of every entry point must agree bitwise."""
+    cfg = synth.CONFIGS[name]
+    if name in ("medium", "large"):
+        cfg = cfg.with_(D=32)
+    x = np.stack([synth.datacube(cfg, i) for i in range(2)])
+    st = synth.steering(cfg, "random")
+    plan = plan_for(stap, cfg, batch=2)
+    dc, ds = dev(x).reshape(plan.cube_shape), dev(st)
+    y0, i0 = plan.run(dc, ds)
+    c0 = plan.covariance(dc)
+    w0, g0, j0 = plan.solve_weights(c0, ds)
+    a0 = plan.apply(dc, w0)
+    for _ in range(8):
+        y, i = plan.run(dc, ds)
+        c = plan.covariance(dc)
+        w, g, j = plan.solve_weights(c, ds)
+        a = plan.apply(dc, w)
+        assert torch.equal(y, y0) and torch.equal(i, i0)
+        assert torch.equal(c, c0) and torch.equal(w, w0) and torch.equal(g, g0) and torch.equal(j, j0)
+        assert torch.equal(a, a0)
+
+
+def test_wrap_only_window_shard(stap):
+    """A shard whose whole window wraps around the cube edge (bins D-1, 0, 1, ...)."""
+    cfg = synth.CONFIGS["small"]
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    _, Yfull, _ = run_gpu(stap, cfg, cube, st)
+    lo, cnt = 0, 3
+    b0, nb = synth.shard_window(cfg, lo, cnt)
+    assert b0 == cfg.D - cfg.h
+    local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
+    _, Y, _ = run_gpu(stap, cfg, local, st, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb)
+    assert np.array_equal(Y[0], Yfull[0, lo:lo + cnt])
