@@ -94,20 +94,12 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       if (!ok && !fail) fail = j + 1;
       if (!ok) x = 1.0f;
       const float r = rsqrtf(x);  // one MUFU on the pivot chain
-      const float d = x * r;
       if (gl == 0) sh.rdiag[j] = r;
+      // column j is published RAW (consumers scale by r); the owners keep it raw
+      // and scale their whole L once after the factorisation (no per-row branch here)
       if (q == qq) {
 #pragma unroll
-        for (int u = CF::umin(v); u < MR; ++u) {
-          const int i = PR * u + p;
-          if (i > j) {
-            A[u][v].x *= r;
-            A[u][v].y *= r;
-            sh.col[i] = A[u][v];
-          } else if (i == j) {
-            A[u][v] = make_float2(d, 0.f);
-          }
-        }
+        for (int u = CF::umin(v); u < MR; ++u) sh.col[PR * u + p] = A[u][v];
       }
       if (p == pj) {
 #pragma unroll
@@ -126,9 +118,15 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       // (c) rank-1 update of the trailing matrix and of the right-hand sides
       float2 Li[MR], Ll[MC], yk[SC];
 #pragma unroll
-      for (int u = CF::umin(v); u < MR; ++u) Li[u] = sh.col[PR * u + p];
+      for (int u = CF::umin(v); u < MR; ++u) {
+        const float2 c = sh.col[PR * u + p];
+        Li[u] = make_float2(c.x * r, c.y * r);  // L[i][j]
+      }
 #pragma unroll
-      for (int v2 = v; v2 < MC; ++v2) Ll[v2] = sh.col[PC * v2 + q];
+      for (int v2 = v; v2 < MC; ++v2) {
+        const float2 c = sh.col[PC * v2 + q];
+        Ll[v2] = make_float2(c.x * r, c.y * r);  // L[l][j]
+      }
 #pragma unroll
       for (int kv = 0; kv < SC; ++kv) yk[kv] = sh.yb[PC * kv + q];
       // Only lower-triangle entries right of column j must change; the others a
@@ -150,6 +148,17 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
           for (int kv = 0; kv < SC; ++kv) cmsub(B[u][kv], Li[u], yk[kv]);
         }
       }
+    }
+  }
+  // deferred column scaling: L[i][l] = raw[i][l] / sqrt(pivot_l) for every held entry
+  // (diagonal and upper-triangle entries become garbage: the back solve never reads them)
+#pragma unroll
+  for (int v = 0; v < MC; ++v) {
+    const float rl = sh.rdiag[(PC * v + q) < N ? PC * v + q : 0];
+#pragma unroll
+    for (int u = CF::umin(v); u < MR; ++u) {
+      A[u][v].x *= rl;
+      A[u][v].y *= rl;
     }
   }
 
