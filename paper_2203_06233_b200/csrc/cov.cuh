@@ -211,50 +211,66 @@ __global__ void __launch_bounds__(256, ((C & 1) && C >= 5) ? 1 : 2) cov_kernel(K
   if (tid < Prun) delta_s[tid] = delta_from_blocks(blk, C, T, N, p.lam, tid);
   __syncthreads();
 
-  // Assemble R_d for each bin of the run (both triangles; lower = conj of upper):
-  // a warp writes RPW = 32 / NP whole rows per iteration (NP = column pairs per
-  // row), one column pair per lane (16-byte stores); a lane's row slot and its
-  // columns' (t_l, c_l) split are computed once.
+  // Assemble R_d for each bin of the run (both triangles; lower = conj of upper).
+  // R_d is T x T tiles of C x C; tile (ti, tl) is lag block (pr + min, |tl - ti|),
+  // conjugate-transposed below the diagonal.  A lane owns one element pair
+  // (ci, 2cp..2cp+1) of a tile (fixed for the whole loop); a warp covers
+  // 32 / (C * ceil(C/2)) tiles per pass, so the index math is per tile, not per element.
+  constexpr int CP = (C + 1) / 2;  // element pairs per tile row
+  constexpr int LPT = C * CP;      // lanes per tile
+  constexpr int TPW = 32 / LPT;    // tiles per warp pass
   const long long NN = (long long)N * N;
   float2* out = cov + (((long long)n * p.dop_count + dl0) * p.B + b) * NN;
   const long long ostride = (long long)p.B * NN;  // between consecutive bins
   const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int NP = (N + 1) >> 1;
-  const int RPW = NP >= 32 ? 1 : 32 / NP;
-  const int slot = lane / NP, pair = lane - slot * NP;
-  const bool lane_on = slot < RPW && pair < NP;
-  const int colA = 2 * pair, colB = 2 * pair + 1;
-  const int tA = colA / C, cA = colA - tA * C, tB = colB / C, cB = colB - tB * C;
-  const bool vec = (N & 1) == 0;
-  const int rows = Prun * N;
-  for (int row0 = warp * RPW; row0 < rows; row0 += nwarps * RPW) {
-    const int row = row0 + slot;
-    if (!lane_on || row >= rows) continue;
-    const int pr = row / N, i = row - pr * N;
-    const int ti = i / C, ci = i - ti * C;
-    const float dl = delta_s[pr];
-    float2 v[2];
+  const int slot = lane / LPT, e = lane - slot * LPT;
+  const int ci = e / CP, c0 = 2 * (e - (e / CP) * CP);
+  const bool two = c0 + 1 < C;
+  const int TT = T * T, ntiles = Prun * TT, bsd = blk_stride(C);
+  for (int t0 = warp * TPW; t0 < ntiles; t0 += nwarps * TPW) {
+    const int t = t0 + slot;
+    if (slot >= TPW || t >= ntiles) continue;
+    const int pr = t / TT, rem = t - pr * TT;
+    const int ti = rem / T, tl = rem - ti * T;
+    float2 v0, v1;
+    if (ti < tl) {
+      const float2* s = blk + lag_block_index(pr + ti, tl - ti, W) * bsd + ci * C + c0;
+      v0 = s[0];
+      v1 = two ? s[1] : make_float2(0.f, 0.f);
+    } else if (ti > tl) {
+      const float2* s = blk + lag_block_index(pr + tl, ti - tl, W) * bsd + c0 * C + ci;
+      const float2 u0 = s[0], u1 = two ? s[C] : make_float2(0.f, 0.f);
+      v0 = make_float2(u0.x, -u0.y);
+      v1 = make_float2(u1.x, -u1.y);
+    } else {  // diagonal tile: upper from the block, lower mirrored, loading on the diagonal
+      const float2* s = blk + lag_block_index(pr + ti, 0, W) * bsd;
+      const float dl = delta_s[pr];
+      float2 x[2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int col = e ? colB : colA, tl = e ? tB : tA, cl = e ? cB : cA;
-      float2 x = make_float2(0.f, 0.f);
-      if (col < N) {
-        if (ti < tl || (ti == tl && ci <= cl)) {
-          x = blk[lag_block_index(pr + ti, tl - ti, W) * blk_stride(C) + ci * C + cl];
-        } else {
-          const float2 u = blk[lag_block_index(pr + tl, ti - tl, W) * blk_stride(C) + cl * C + ci];
-          x = make_float2(u.x, -u.y);
+      for (int q2 = 0; q2 < 2; ++q2) {
+        const int cl = c0 + q2;
+        if (q2 == 1 && !two) {
+          x[q2] = make_float2(0.f, 0.f);
+          continue;
         }
-        if (col == i) x = make_float2(x.x + dl, 0.f);
+        if (ci < cl) {
+          x[q2] = s[ci * C + cl];
+        } else if (ci > cl) {
+          const float2 u = s[cl * C + ci];
+          x[q2] = make_float2(u.x, -u.y);
+        } else {
+          x[q2] = make_float2(s[ci * C + ci].x + dl, 0.f);
+        }
       }
-      v[e] = x;
+      v0 = x[0];
+      v1 = x[1];
     }
-    float2* orow = out + pr * ostride + (long long)i * N;
-    if (vec) {
-      *reinterpret_cast<float4*>(orow + colA) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    float2* o = out + pr * ostride + (long long)(ti * C + ci) * N + tl * C + c0;
+    if ((C & 1) == 0) {
+      *reinterpret_cast<float4*>(o) = make_float4(v0.x, v0.y, v1.x, v1.y);  // N even: 16-byte aligned
     } else {
-      orow[colA] = v[0];
-      if (colB < N) orow[colB] = v[1];
+      o[0] = v0;
+      if (two) o[1] = v1;
     }
   }
 }
