@@ -320,9 +320,12 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
       if (2048 / threads < cta_per_sm) cta_per_sm = 2048 / threads;
       if (cta_per_sm < 1) break;
       const int warps = cta_per_sm * threads / 32;
-      // prefer more resident warps and CTAs (independent phases overlap), then
-      // less covariance work per bin (larger P)
-      const double score = (warps > 32 ? 32 : warps) * 1000.0 + cta_per_sm * 100.0 + P;
+      // solver segments work in rounds of ng bins: the last round of a run of P
+      // bins is P mod ng busy, so weight by the round balance
+      const double balance = (double)P / ((double)((P + ng - 1) / ng) * ng);
+      // prefer more busy resident warps and CTAs (independent phases overlap),
+      // then less covariance work per bin (larger P)
+      const double score = (warps > 32 ? 32 : warps) * balance * 1000.0 + cta_per_sm * 10.0 + P * 0.01;
       if (score > bestScore) {
         bestScore = score;
         bestP = P;
@@ -331,8 +334,8 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
       }
     }
   }
-  // the fused kernel only pays with enough resident warps to overlap its phases
-  // (>= 12 per SM) and when the lag blocks keep >= 1/3 of the threads busy
+  // the fused kernel only pays with enough busy resident warps to overlap its
+  // phases (>= 12 per SM) and when the lag blocks keep >= 1/3 of the threads busy
   if (bestP == 0 || bestScore < 12000.0 || 3 * cov_tpb(kp.C) * cov_blocks(kp.T, bestP + kp.T - 1) < bestT)
     return false;
   f->C = kp.C;
