@@ -31,7 +31,8 @@ __host__ __device__ inline int cov_blocks(int T, int W) { return T * W - T * (T 
 // staged lag-block stride (complex): C*C + 1 so the same element of consecutive blocks
 // falls on different banks (the HERK writes and the R assembly reads are conflict-free)
 __host__ __device__ inline int blk_stride(int C) { return C * C + 1; }
-__host__ __device__ inline int cov_tpb(int C) { return (C >= 4 && (C & 1) == 0) ? 2 : 1; }  // threads per block
+// threads per lag block: C=4 -> 4 (one row each), other even C >= 6 -> 2 (C/2 rows), odd C -> 1
+__host__ __device__ constexpr int cov_tpb(int C) { return C == 4 ? 4 : ((C >= 6 && (C & 1) == 0) ? 2 : 1); }
 __host__ __device__ inline int tile_rs(int KC) { return KC + 2; }                             // row stride (complex)
 __host__ __device__ inline int tile_bs(int C, int KC) { return C * (KC + 2) + 2; }            // bin stride (complex)
 // largest even divisor of K that is <= 32
@@ -138,7 +139,7 @@ template <int C>
 __device__ __forceinline__ void cta_lag_blocks(const KParams& p, const float2* __restrict__ cube, int n, int b,
                                                int d0, int W, const CovLayout& L, unsigned char* tiles,
                                                uint64_t* bar, float2* blk) {
-  constexpr int TPB = (C >= 4 && (C & 1) == 0) ? 2 : 1;
+  constexpr int TPB = cov_tpb(C);
   constexpr int TI = C / TPB;
   const int tid = threadIdx.x;
   const int T = p.T;
