@@ -1,5 +1,5 @@
 """Write profiles/<tag>_ncu_summary.txt and update profiles/traffic.json from an ncu --set full report.
-Usage: python profiles/make_summary.py <report.ncu-rep> <tag> <workload key> <launches per capture>"""
+Usage: python profiles/make_summary.py <report.ncu-rep> <tag> <workload key> [kernel substring for the traffic entry]"""
 import csv, io, json, os, subprocess, sys
 
 rep, tag, key = sys.argv[1], sys.argv[2], sys.argv[3]
@@ -40,6 +40,8 @@ for r in rows[2:]:
 open(os.path.join(HERE, f"{tag}_ncu_summary.txt"), "w").write("\n".join(lines) + "\n")
 tj = os.path.join(HERE, "traffic.json")
 data = json.load(open(tj)) if os.path.exists(tj) else {}
-data[key] = {"bytes_per_launch": max(traffic.values()), "kernel": max(traffic, key=traffic.get), "report": tag}
+sel = [k for k in traffic if len(sys.argv) > 4 and sys.argv[4] in k] or list(traffic)
+kern = max(sel, key=traffic.get)
+data[key] = {"bytes_per_launch": traffic[kern], "kernel": kern, "report": tag}
 json.dump(data, open(tj, "w"), indent=1)
 print("\n".join(lines))
