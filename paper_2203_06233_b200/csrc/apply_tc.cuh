@@ -1,0 +1,435 @@
+// apply_tc.cuh -- K3 on the 5th-generation tensor cores (tcgen05.mma kind::tf32)
+// with a 3xTF32 split so the result keeps FP32 accuracy.  Used by the staged path
+// when S = 16, K % 64 == 0 and N <= 64 (medium / large); the SIMT apply (apply.cuh)
+// covers every other shape.
+//
+// Method: Y[d][k][r] = w_{d,b(r),k}^H z_{d,r} (reading c-12; PAPER.md "Beamforming"
+// / Fig. 1 "apply weights"), written as one real GEMM per tile of 64 range cells of
+// a unit (d, b):
+//   rows    m = 2*jj + part, jj < 64 the cell, part 0 = Re z, 1 = Im z   -> M = 128
+//   columns n < S: Re w_k,  n >= S: Im w_{n-S}                          -> N = 2S = 32
+//   reduction i = snapshot element t*C + c, zero-padded to 8*KS         -> K = 8 per MMA
+//   Out[m][n] = sum_i A[m][i] B[n][i],  A[2jj+p][i] = part_p(z_i[jj]),  B as above
+//   Re Y[k][jj] = Out[2jj][k] + Out[2jj+1][S+k],  Im Y[k][jj] = Out[2jj+1][k] - Out[2jj][S+k]
+// 3xTF32: x = hi + lo, hi = x rounded to TF32, lo = x - hi (exact; |lo| <= 2^-12 |x|, the
+//   tensor core truncates it to TF32, error <= 2^-23 |x|);
+//   A B ~= Ahi Bhi + Ahi Blo + Alo Bhi (the dropped Alo Blo is <= 2^-24 |A||B|),
+//   FP32 accumulation in tensor memory.
+//
+// Data movement (B200-first):
+//   * A (the snapshots, 128 x 8KS): the N rows of a tile are T boxes of {64 cells, C
+//     channels} of the cube; one thread TMA-loads them (cp.async.bulk.tensor.2d) into a
+//     ring of ns shared-memory stages on mbarriers.  The two warps of TMEM lane
+//     quarter q read the (cell, part) columns m = 32q + lane of the stage
+//     (conflict-free), split them and write TMEM lane m (half of the k-steps each)
+//     with tcgen05.st;
+//     the MMA reads A from TMEM (the "TS" form), so the dominant operand needs no
+//     transpose and its hi/lo copies cost no shared-memory bandwidth.
+//   * B (the weights: 32 hi rows then 32 lo rows x 8KS) goes to shared memory in the
+//     canonical K-major no-swizzle layout (8-row x 16-byte core matrices: LBO = 128 B between the two
+//     4-element halves of an MMA k-step, SBO = 256 B between 8-row groups).
+//   * Warp-specialised pipeline, two persistent CTAs per SM (10 warps and 256 TMEM
+//     columns each): a producer warp issues the TMA loads into the stage ring
+//     (full/empty mbarriers); an MMA warp issues a tile's 2*KS MMAs once the 8 compute
+//     warps have written its A and B (a_full) and commits to mma_bar; the accumulator
+//     is double-buffered, so the compute warps drain tile j-1 while the MMAs of tile j
+//     run.  (A 1-CTA/SM variant with 16 compute warps and double-buffered A measured
+//     slower: more per-warp overhead, one pipeline per SM.)
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace stapk {
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: start, leading / stride byte offsets (>>4), version 1
+// (sm_100), base offset 0, no swizzle.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N, M
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
+  return (1u << 4)                       // c_format = F32
+         | (2u << 7)                     // a_format = TF32
+         | (2u << 10)                    // b_format = TF32
+         | ((uint32_t)(N >> 3) << 17)    // n_dim
+         | ((uint32_t)(M >> 4) << 24);   // m_dim
+}
+
+// D[tmem d] (+)= A[tmem a] * B[smem desc b]^T
+__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 consecutive fp32 columns of this warp's 32 TMEM lanes (one lane per thread)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// two runs of 8 consecutive fp32 columns of this warp's 32 TMEM lanes, with the wait in
+// the same asm block so no use of the results can be scheduled before it
+__device__ __forceinline__ void tmem_ld8x2(uint32_t ta, uint32_t tb, float (&va)[8], float (&vb)[8]) {
+  uint32_t a[8], b[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%17];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]),
+        "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]), "=r"(b[7])
+      : "r"(ta), "r"(tb)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    va[i] = __uint_as_float(a[i]);
+    vb[i] = __uint_as_float(b[i]);
+  }
+}
+
+// four runs of 8 consecutive fp32 columns of this warp's 32 TMEM lanes, wait included
+__device__ __forceinline__ void tmem_ld8x4(uint32_t ta, uint32_t tb, uint32_t tc, uint32_t td, float (&va)[8],
+                                           float (&vb)[8], float (&vc)[8], float (&vd)[8]) {
+  uint32_t a[8], b[8], c[8], d[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%32];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%33];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%34];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%35];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]),
+        "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]), "=r"(b[7]),
+        "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]), "=r"(c[6]), "=r"(c[7]),
+        "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+      : "r"(ta), "r"(tb), "r"(tc), "r"(td)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    va[i] = __uint_as_float(a[i]);
+    vb[i] = __uint_as_float(b[i]);
+    vc[i] = __uint_as_float(c[i]);
+    vd[i] = __uint_as_float(d[i]);
+  }
+}
+
+// four runs of 4 consecutive fp32 columns of this warp's 32 TMEM lanes, wait included
+__device__ __forceinline__ void tmem_ld4x4(uint32_t ta, uint32_t tb, uint32_t tc, uint32_t td, float (&va)[4],
+                                           float (&vb)[4], float (&vc)[4], float (&vd)[4]) {
+  uint32_t a[4], b[4], c[4], d[4];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [%17];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [%18];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [%19];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]),
+        "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(ta), "r"(tb), "r"(tc), "r"(td)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    va[i] = __uint_as_float(a[i]);
+    vb[i] = __uint_as_float(b[i]);
+    vc[i] = __uint_as_float(c[i]);
+    vd[i] = __uint_as_float(d[i]);
+  }
+}
+
+// 8 consecutive fp32 columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+// 2-D TMA tile load (no swizzle) of box {x.., y..} of *map into dst, completing on bar
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// round x to TF32 (10-bit mantissa, ties away from zero) with integer ops: adding half
+// a TF32 ulp to the magnitude bits and truncating; the low 13 bits are 0
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+constexpr int kApplyTcComputeWarps = 8;                        // 2 per TMEM lane quarter
+constexpr int kApplyTcThreads = kApplyTcComputeWarps * 32 + 64;  // + producer warp + MMA warp
+constexpr int kApplyTcTmemCols = 256;  // A hi [0,64) | A lo [64,128) | accumulators x 2 [128,256)
+constexpr int kApplyTcSmemBudget = 112 * 1024;  // two CTAs per SM
+
+// shared memory: B (KS k-steps x 64 rows x 32 B: rows 0-31 hi, 32-63 lo) | ns stages |
+// barriers.  A stage holds the N snapshot rows of a tile (512 B
+// each) and, for a unit's first tile, its S x N weights.
+__host__ __device__ inline uint32_t apply_tc_b_bytes(int KS) { return (uint32_t)KS * 2048u; }
+__host__ __device__ inline uint32_t apply_tc_stage_bytes(int N) { return (uint32_t)N * (512u + 16u * 8u); }
+__host__ inline int apply_tc_stages(int N) {
+  const int KS = (N + 7) / 8;
+  const int ns = (int)((kApplyTcSmemBudget - apply_tc_b_bytes(KS) - 512) / apply_tc_stage_bytes(N));
+  return ns < 2 ? 2 : ns > 8 ? 8 : ns;
+}
+__host__ inline size_t apply_tc_smem_bytes(int N) {
+  const int KS = (N + 7) / 8;
+  const size_t need = (size_t)apply_tc_b_bytes(KS) + (size_t)apply_tc_stages(N) * apply_tc_stage_bytes(N) + 512;
+  return need < 80 * 1024 ? 80 * 1024 : need;  // >= 80 KB caps residency at 2 CTAs per SM (TMEM)
+}
+__host__ inline bool apply_tc_supported(int N, int S, int K) { return S == 16 && K % 64 == 0 && N >= 1 && N <= 64; }
+
+// Two CTAs per SM, each walking units u = blockIdx.x, +gridDim.x, ...; a unit is K/64
+// tiles of 64 cells.  Tile j of the CTA uses stage j % ns and accumulator j & 1.  Per
+// k-step two MMAs: Ahi x [Bhi; Blo] (N = 64) into
+// accumulator columns [0,64) and Alo x Bhi (N = 32) into [0,32); the epilogue adds
+// column c and c + 32.
+template <int KS>
+__global__ void __launch_bounds__(kApplyTcThreads, 2)
+    apply_tc_kernel(const __grid_constant__ CUtensorMap cube_map, KParams p, const float2* __restrict__ wts,
+                    float2* __restrict__ out, int units, int ns) {
+  constexpr int S = 16, NP = 8 * KS;
+  constexpr int kCompute = kApplyTcComputeWarps * 32;
+  extern __shared__ __align__(128) unsigned char smem[];  // no-swizzle descriptors need 16 B
+  const int N = p.N, K = p.K, C = p.C, D = p.D, R = p.R;
+  unsigned char* bbuf = smem;
+  unsigned char* stage0 = smem + apply_tc_b_bytes(KS);
+  const uint32_t stage_bytes = apply_tc_stage_bytes(N);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + (size_t)ns * stage_bytes);  // stage loaded
+  uint64_t* empty = full + ns;                                                      // stage read
+  uint64_t* a_full = empty + ns;   // A (TMEM) and B (smem) of the tile written
+  uint64_t* mma_bar = a_full + 1;  // the tile's MMAs done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kApplyTcTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCompute);
+    }
+    mbar_init(a_full, kCompute);
+    mbar_init(mma_bar, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int MT = K / 64;
+  const int G = gridDim.x;
+  const int my_units = (int)blockIdx.x < units ? (units - (int)blockIdx.x + G - 1) / G : 0;
+  const int ntiles = my_units * MT;
+  const int Gq = G / p.B, Gr = G - Gq * p.B;
+
+  struct Tile {
+    int u, mt, b, nd, q;  // unit, 64-cell tile in the unit, block, (cube, bin) row, unit count
+  };
+  Tile t;  // this warp's current tile
+  t.u = (int)blockIdx.x;
+  t.mt = 0;
+  t.nd = t.u / p.B;
+  t.b = t.u - t.nd * p.B;
+  t.q = 0;
+  auto advance = [&](Tile& x) {  // this CTA's next tile: next 64 cells, else unit u + G
+    if (++x.mt == MT) {
+      x.mt = 0;
+      x.u += G;
+      ++x.q;
+      x.nd += Gq;
+      x.b += Gr;
+      if (x.b >= p.B) {
+        x.b -= p.B;
+        ++x.nd;
+      }
+    }
+  };
+
+  if (warp == kApplyTcComputeWarps) {
+    // ---- producer (one thread): per tile, TMA-load the N snapshot rows -- per lag t one
+    // {64 cells, C channels} box of the cube viewed as [batch*nbins*C rows][2R floats] --
+    // and, for a unit's first tile, bulk-copy its S x N weights; all complete on full[s]
+    if (lane == 0) {
+      const uint32_t wbytes = (uint32_t)(S * N * 8);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        if (j >= ns) mbar_wait(&empty[s], ph ^ 1u);  // the compute warps have read tile j - ns
+        const int n = t.nd / p.dop_count, d = p.dop_begin + (t.nd - n * p.dop_count);
+        const int base = local_bin(p, d - p.h);  // local row of bin d-h; the window wraps mod D
+        unsigned char* dst = stage0 + (size_t)s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)N * 512u + (t.mt == 0 ? wbytes : 0u));
+        if (t.mt == 0) bulk_g2s(dst + (size_t)N * 512, wts + (long long)t.u * S * N, wbytes, &full[s]);
+        const int x = 2 * (t.b * K + t.mt * 64), y0 = n * p.nbins * C;
+        for (int tt = 0; tt < p.T; ++tt) {
+          int lb = base + tt;
+          lb -= lb >= D ? D : 0;
+          tma_load_2d(dst + (size_t)tt * C * 512, &cube_map, x, y0 + lb * C, &full[s]);
+        }
+        advance(t);
+        if (++s == ns) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == kApplyTcComputeWarps + 1) {
+    // ---- MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t id64 = umma_idesc_tf32(128, 64), id32 = umma_idesc_tf32(128, 32);
+      for (int j = 0; j < ntiles; ++j) {
+        mbar_wait(a_full, (uint32_t)j & 1u);
+        tc_fence_after();
+        const uint32_t bb = smem_u32(bbuf);
+        const uint32_t acc = tmem + 128 + 64 * (j & 1), ahi = tmem, alo = tmem + 64;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint64_t bd = umma_desc(bb + ks * 2048, 128, 256);
+          umma_tf32_ts(acc, ahi + 8 * ks, bd, id64, ks > 0);  // Ahi x [Bhi; Blo]
+          umma_tf32_ts(acc, alo + 8 * ks, bd, id32, 1);       // Alo x Bhi (rows 0-31 of B)
+        }
+        umma_commit(mma_bar);
+      }
+    }
+  } else {
+    // ---- compute warps: warp w owns TMEM lane quarter q4 = w % 4 (rows m = 32 q4 + lane),
+    // k-steps hq, hq + 2, ... (hq = w / 4) of A, and steering k in [8hq, 8hq + 8)
+    const int q4 = warp & 3, hq = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const int m = q4 * 32 + lane, jj = m >> 1, part = m & 1;
+    constexpr int KH = (KS + 1) / 2;  // k-steps per warp (at most)
+
+    // weights (in the stage) -> B buffer: K-major rows nn = lo*32 + part*16 + k, column i
+    auto stage_b = [&](const float2* wg, unsigned char* bb) {
+      const int i3 = lane & 3, k7 = lane >> 2;  // a warp stores 128 contiguous bytes
+      for (int g = warp; g < 2 * (NP / 4); g += kApplyTcComputeWarps) {
+        const int i = (g >> 1) * 4 + i3, k = (g & 1) * 8 + k7;
+        const float2 w = i < N ? wg[k * N + i] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          const int nn = pp * S + k;
+          const float x = pp ? w.y : w.x;
+          const float hi = tf32_hi(x);
+          const uint32_t off =
+              (uint32_t)(i >> 3) * 2048u + (nn >> 3) * 256 + ((i >> 2) & 1) * 128 + (nn & 7) * 16 + (i & 3) * 4;
+          *reinterpret_cast<float*>(bb + off) = hi;
+          *reinterpret_cast<float*>(bb + off + 4 * 256) = x - hi;  // row nn + 32
+        }
+      }
+    };
+    // accumulator of tile x (parity par) -> Y[k][cell] for k in [8hq, 8hq+8)
+    auto epilogue = [&](const Tile& x, int par) {
+      float a[8], b[8], c[8], d[8];
+      const uint32_t acc = tmem + lane_base + 128 + 64 * par + 8 * hq;
+      tmem_ld8x4(acc, acc + S, acc + 32, acc + 32 + S, a, b, c, d);
+      float* yf =
+          reinterpret_cast<float*>(out + (long long)x.nd * S * R + (long long)x.b * K + x.mt * 64 + jj) + part;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float re = a[k] + c[k];                                  // Out[m][k]
+        const float o = __shfl_xor_sync(0xffffffffu, b[k] + d[k], 1);  // partner row's Out[.][S+k]
+        yf[(long long)(8 * hq + k) * R * 2] = part ? (re - o) : (re + o);  // Re: own+partner; Im: own-partner
+      }
+    };
+
+    Tile prev = t;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int j = 0; j < ntiles; ++j) {
+      const float* zs = reinterpret_cast<const float*>(stage0 + (size_t)s * stage_bytes) + m;
+      mbar_wait(&full[s], ph);
+      float z[KH][8];
+#pragma unroll
+      for (int kh = 0; kh < KH; ++kh)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = 8 * (hq + 2 * kh) + e;
+          z[kh][e] = (i < N && hq + 2 * kh < KS) ? zs[i * 128] : 0.f;
+        }
+      if (j >= 1) {  // MMA(j-1) done: A, B and accumulator (j-1) & 1 are ready
+        mbar_wait(mma_bar, (uint32_t)(j - 1) & 1u);
+        tc_fence_after();
+      }
+      if (t.mt == 0) {
+        stage_b(reinterpret_cast<const float2*>(stage0 + (size_t)s * stage_bytes + (size_t)N * 512), bbuf);
+        fence_proxy_async();  // generic-proxy B stores -> visible to the tensor core
+      }
+      mbar_arrive(&empty[s]);  // this thread is done with stage s
+      // A: row m, k-steps hq + 2kh: hi at column 8ks, lo at 64 + 8ks
+#pragma unroll
+      for (int kh = 0; kh < KH; ++kh) {
+        const int ks = hq + 2 * kh;
+        if (ks < KS) {
+          float h[8], l[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            h[e] = tf32_hi(z[kh][e]);
+            l[e] = z[kh][e] - h[e];
+          }
+          tmem_st8(tmem + lane_base + 8 * ks, h);
+          tmem_st8(tmem + lane_base + 64 + 8 * ks, l);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(a_full);
+      if (j >= 1) {  // drain tile j-1 while MMA(j) runs
+        epilogue(prev, (j - 1) & 1);
+        tc_fence_before();
+      }
+      prev = t;
+      advance(t);
+      if (++s == ns) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    if (ntiles > 0) {
+      const int jl = ntiles - 1;
+      mbar_wait(mma_bar, (uint32_t)jl & 1u);
+      tc_fence_after();
+      epilogue(prev, jl & 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kApplyTcTmemCols));
+}
+
+}  // namespace stapk

@@ -5,12 +5,16 @@
 // of cov.cuh (K1), solve.cuh (K2), apply.cuh (K3) and fused.cuh (K4).  There
 // is no CPU path: without an sm_100 device every call returns an error.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/stap.h"
 #include "apply.cuh"
+#include "apply_tc.cuh"
 #include "cov.cuh"
 #include "fused.cuh"
 #include "solve.cuh"
@@ -32,6 +36,8 @@ struct stap_plan {
   size_t solve_smem;
   // K3
   int apply_tpu, apply_upc, apply_smax, apply_grid;
+  int apply_tc, apply_tc_grid, apply_tc_ns;  // tcgen05 3xTF32 apply (apply_tc.cuh) when supported
+  size_t apply_tc_smem;
   size_t apply_smem;
   // K4 (fused) selection
   int fused;  // 1 if stap_run uses the fused kernel
@@ -111,7 +117,65 @@ void apply_launch_t(const stap_plan* pl, const float2* cube, const float2* w, fl
       pl->kp, cube, w, out, pl->apply_tpu, pl->apply_upc, pl->units);
 }
 
+// cuTensorMapEncodeTiled from the driver, without linking libcuda
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// the cube as a 2-D fp32 tensor [batch*nbins*C rows][2R floats], box {128 floats, C rows}
+bool encode_cube_map(const stap_plan* pl, const float2* cube, CUtensorMap* map) {
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const KParams& k = pl->kp;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * k.R, (cuuint64_t)k.batch * k.nbins * k.C};
+  const cuuint64_t strides[1] = {(cuuint64_t)k.R * 8};
+  const cuuint32_t box[2] = {128, (cuuint32_t)k.C}, estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(cube), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int KS>
+void apply_tc_launch_t(const stap_plan* pl, const CUtensorMap& map, const float2* w, float2* out, cudaStream_t st) {
+  apply_tc_kernel<KS><<<pl->apply_tc_grid, kApplyTcThreads, pl->apply_tc_smem, st>>>(map, pl->kp, w, out,
+                                                                                      (int)pl->units, pl->apply_tc_ns);
+}
+void apply_tc_attr(int N, size_t smem) {
+  switch ((N + 7) / 8) {
+    case 1: cudaFuncSetAttribute(apply_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 2: cudaFuncSetAttribute(apply_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 3: cudaFuncSetAttribute(apply_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 4: cudaFuncSetAttribute(apply_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 5: cudaFuncSetAttribute(apply_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 6: cudaFuncSetAttribute(apply_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 7: cudaFuncSetAttribute(apply_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 8: cudaFuncSetAttribute(apply_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+  }
+}
+
 void apply_launch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
+  CUtensorMap map;
+  if (pl->apply_tc && encode_cube_map(pl, cube, &map)) {  // (an unaligned cube view takes the SIMT kernel)
+    switch ((pl->kp.N + 7) / 8) {
+      case 1: apply_tc_launch_t<1>(pl, map, w, out, st); break;
+      case 2: apply_tc_launch_t<2>(pl, map, w, out, st); break;
+      case 3: apply_tc_launch_t<3>(pl, map, w, out, st); break;
+      case 4: apply_tc_launch_t<4>(pl, map, w, out, st); break;
+      case 5: apply_tc_launch_t<5>(pl, map, w, out, st); break;
+      case 6: apply_tc_launch_t<6>(pl, map, w, out, st); break;
+      case 7: apply_tc_launch_t<7>(pl, map, w, out, st); break;
+      case 8: apply_tc_launch_t<8>(pl, map, w, out, st); break;
+    }
+    return;
+  }
   switch (pl->apply_smax) {
     case 2: apply_launch_t<2>(pl, cube, w, out, st); break;
     case 4: apply_launch_t<4>(pl, cube, w, out, st); break;
@@ -277,6 +341,17 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   pl->apply_smax = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <= 16 ? 16 : 32;
   pl->apply_smem = apply_smem_bytes(N, pl->apply_smax, pl->apply_upc);
   pl->apply_grid = (int)((pl->units + pl->apply_upc - 1) / pl->apply_upc);
+  {
+    const char* e = getenv("STAP_APPLY_SIMT");  // developer A/B knob
+    pl->apply_tc =
+        (apply_tc_supported(N, S, K) && pl->units < (1LL << 30) && tensor_map_encoder() && !(e && atoi(e))) ? 1 : 0;
+    pl->apply_tc_ns = apply_tc_stages(N);
+    pl->apply_tc_smem = apply_tc_smem_bytes(N);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+    const long long g = 2LL * nsm;  // persistent: two CTAs per SM, each walking whole units
+    pl->apply_tc_grid = (int)(pl->units < g ? pl->units : g);
+  }
 
   // K4: fused single-kernel path when it fits
   pl->fused = fused_configure(kp, &pl->fcfg) ? 1 : 0;
@@ -308,6 +383,8 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
     else
       solve_set_attr(pl->solve_sel, pl->solve_smem);
     set_apply_attr(pl->apply_smax, pl->apply_smem);
+    if (pl->apply_tc)
+      apply_tc_attr(N, pl->apply_tc_smem);
     if (pl->fused) fused_set_attr(pl->fcfg);
     if (cudaGetLastError() != cudaSuccess) {
       delete pl;
@@ -317,9 +394,9 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   if (pl->fused)
     snprintf(pl->desc, sizeof pl->desc, "fused:%s", pl->fcfg.name);
   else
-    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(tpu=%d,upc=%d)",
+    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(%s,tpu=%d,upc=%d)",
              pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
-             pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tpu,
+             pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
              pl->apply_upc);
   *out_plan = pl;
   return STAP_OK;

@@ -199,7 +199,8 @@ def test_fused_equals_staged(stap, name):
     _, Yf, If = run_gpu(stap, cfg, cube, st)
     res = run_gpu(stap, cfg, cube, st, staged=True)
     assert np.array_equal(If, res[2])
-    assert rel_lines(Yf, res[1]).max() <= 1e-5
+    e = rel_lines(Yf, res[1]).max()
+    assert e <= 1e-5, e
 
 
 @pytest.mark.parametrize("name,G", [("tiny", 3), ("small", 2), ("small", 8), ("medium", 4)])
