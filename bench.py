@@ -250,7 +250,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(WORKLOAD_DESC), default="small")
     ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
-    ap.add_argument("--path", choices=["auto", "staged"], default="auto")
+    ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto",
+                    help="stap_run path (stap_params.path); auto = the library's measured choice")
     ap.add_argument("--gather", action="store_true", help="NCCL all-gather of outputs after each step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -285,13 +286,13 @@ def main():
     M = args.cubes
     dims = stap.Dims(cfg.C, cfg.T, gcfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
     plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                         device=local_rank)
+                         device=local_rank, path=args.path)
     stream = torch.cuda.current_stream(dev)
     cube = torch.from_numpy(x_h).to(dev)
     steer = torch.from_numpy(st_h).to(dev)
     out = torch.empty(plan.out_shape, dtype=torch.complex64, device=dev)
     info = torch.empty(plan.info_shape, dtype=torch.int32, device=dev)
-    staged = args.path == "staged" or plan.description.startswith("staged")
+    staged = plan.description.startswith("staged")
     if staged:
         cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=dev)
         wts = torch.empty(plan.weights_shape, dtype=torch.complex64, device=dev)

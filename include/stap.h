@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define STAP_ABI_VERSION 1
+#define STAP_ABI_VERSION 2
 
 typedef struct { float re, im; } stap_c64;
 typedef struct stap_plan stap_plan;
@@ -85,7 +85,14 @@ typedef struct {
                                 and must cover every owned bin's window                   */
     int32_t batch;           /* independent cubes per call (>= 1), stored back to back     */
     int32_t device;          /* CUDA ordinal the plan launches on                          */
+    int32_t path;            /* stap_run's kernel path, a stap_path value (0 = auto)       */
 } stap_params;
+
+/* stap_run path.  AUTO picks the measured-faster one: the staged path when its
+ * tensor-core apply applies (S = 16, K % 64 == 0, N <= 64), else the fused kernel when
+ * the shape fits it, else staged.  FUSED on a shape the fused kernel cannot hold is
+ * STAP_ERR_UNSUPPORTED.  The stage entry points are independent of this field. */
+typedef enum { STAP_PATH_AUTO = 0, STAP_PATH_FUSED = 1, STAP_PATH_STAGED = 2 } stap_path;
 
 /* Buffer shapes (complex64 unless noted), with B = R/K, N = C*T, Dl = dop_count:
  *   cube     [batch][cube_bins][C][R]

@@ -256,6 +256,7 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   const int C = p->n_chan, T = p->tdof, D = p->n_dop, R = p->n_range, K = p->training_block,
             S = p->n_steering;
   if (C <= 0 || T <= 0 || D <= 0 || R <= 0 || K <= 0 || S <= 0 || p->batch <= 0) return STAP_ERR_BAD_DIMS;
+  if (p->path < STAP_PATH_AUTO || p->path > STAP_PATH_STAGED) return STAP_ERR_BAD_DIMS;
   if (R % K != 0 || T > D) return STAP_ERR_BAD_DIMS;
   if (!(p->diag_load >= 0.0f) || !std::isfinite(p->diag_load)) return STAP_ERR_BAD_DIMS;
   if (p->dop_begin < 0 || p->dop_count <= 0 || (long long)p->dop_begin + p->dop_count > D)
@@ -353,8 +354,15 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
     pl->apply_tc_grid = (int)(pl->units < g ? pl->units : g);
   }
 
-  // K4: fused single-kernel path when it fits
-  pl->fused = fused_configure(kp, &pl->fcfg) ? 1 : 0;
+  // K4: fused single-kernel path when it fits and the caller's path allows it.  AUTO
+  // prefers staged when the tensor-core apply applies (medium, 16 cubes: staged 2.68 ms
+  // vs fused 3.30 ms per step on B200).
+  const bool fits = fused_configure(kp, &pl->fcfg);
+  if (p->path == STAP_PATH_FUSED && !fits) {
+    delete pl;
+    return STAP_ERR_UNSUPPORTED;
+  }
+  pl->fused = (fits && (p->path == STAP_PATH_FUSED || (p->path == STAP_PATH_AUTO && !pl->apply_tc))) ? 1 : 0;
 
   // staged workspace
   const long long NN = (long long)N * N;

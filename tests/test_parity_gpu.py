@@ -69,13 +69,20 @@ def run_gpu(stap, cfg, cube, st, staged=False, **kw):
 
 # ---------------------------------------------------------------- whole path vs oracle
 @pytest.mark.parametrize("name", ["tiny", "small", "medium"])
-@pytest.mark.parametrize("staged", [False, True])
-def test_run_vs_oracle_full(stap, name, staged):
+@pytest.mark.parametrize("mode", ["run-auto", "run-fused", "run-staged", "stages"])
+def test_run_vs_oracle_full(stap, name, mode):
     cfg = synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "ula" if name != "tiny" else "random")
     ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
-    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    staged = mode == "stages"
+    path = mode[4:] if mode.startswith("run-") else "auto"
+    if name == "tiny" and path == "fused":  # below the fused kernel's occupancy floor
+        with pytest.raises(stap.StapError):
+            plan_for(stap, cfg, path="fused")
+        return
+    res = run_gpu(stap, cfg, cube, st, staged=staged, path=path)
+    assert res[0].description.startswith({"fused": "fused", "staged": "staged"}.get(path, ""))
     Y, info = res[1][0], res[2][0]
     err = rel_lines(Y, ref["Y"])
     assert np.array_equal(info, ref["info"])
@@ -190,13 +197,25 @@ def test_E3_target_gpu(stap):
         assert abs(Y[0, d, k, r] - alpha) <= 1e-4 * abs(alpha)
 
 
+def test_path_fused_unsupported(stap):
+    """path=fused on a shape the fused kernel cannot hold is STAP_ERR_UNSUPPORTED; auto picks staged."""
+    cfg = synth.CONFIGS["large"]
+    with pytest.raises(stap.StapError) as e:
+        plan_for(stap, cfg, path="fused")
+    assert e.value.code == 3
+    assert plan_for(stap, cfg).description.startswith("staged")
+    assert plan_for(stap, synth.CONFIGS["medium"]).description.startswith("staged")  # tensor-core apply
+    assert plan_for(stap, synth.CONFIGS["small"]).description.startswith("fused")
+
+
 # ---------------------------------------------------------------- composition, shards, batch, determinism
 @pytest.mark.parametrize("name", ["small", "medium"])
 def test_fused_equals_staged(stap, name):
     cfg = synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "ula")
-    _, Yf, If = run_gpu(stap, cfg, cube, st)
+    pf, Yf, If = run_gpu(stap, cfg, cube, st, path="fused")
+    assert pf.description.startswith("fused")
     res = run_gpu(stap, cfg, cube, st, staged=True)
     assert np.array_equal(If, res[2])
     e = rel_lines(Yf, res[1]).max()
