@@ -84,10 +84,10 @@ __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __r
 #pragma unroll
           for (int k2 = 0; k2 < SMAX / 2; ++k2) {
             const float4 ww = wv[k2];
-            cmac_conja(acc0[2 * k2], make_float2(ww.x, ww.y), z0);
-            cmac_conja(acc1[2 * k2], make_float2(ww.x, ww.y), z1);
-            cmac_conja(acc0[2 * k2 + 1], make_float2(ww.z, ww.w), z0);
-            cmac_conja(acc1[2 * k2 + 1], make_float2(ww.z, ww.w), z1);
+            cmac_conja2(acc0[2 * k2], make_float2(ww.x, ww.y), z0);
+            cmac_conja2(acc1[2 * k2], make_float2(ww.x, ww.y), z1);
+            cmac_conja2(acc0[2 * k2 + 1], make_float2(ww.z, ww.w), z0);
+            cmac_conja2(acc1[2 * k2 + 1], make_float2(ww.z, ww.w), z1);
           }
         }
       }

@@ -80,6 +80,13 @@ __device__ __forceinline__ void cmac_conja(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(a.x, b.y, acc.y);
   acc.y = fmaf(-a.y, b.x, acc.y);
 }
+// acc += conj(w) * z with z as the packed operand and w's parts broadcast (SASS FFMA2
+// with a scalar operand and the LO_HI.NP selector: no pair construction); per
+// component the same two fmaf, same order as cmac_conja(acc, w, z): bit-identical
+__device__ __forceinline__ void cmac_conja2(float2& acc, float2 w, float2 z) {
+  acc = __ffma2_rn(z, make_float2(w.x, w.x), acc);
+  acc = __ffma2_rn(make_float2(z.y, z.x), make_float2(w.y, -w.y), acc);
+}
 // acc -= a * b
 __device__ __forceinline__ void cmsub(float2& acc, float2 a, float2 b) {
   acc.x = fmaf(-a.x, b.x, acc.x);
