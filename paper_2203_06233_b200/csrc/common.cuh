@@ -87,6 +87,24 @@ __device__ __forceinline__ void cmac_conja2(float2& acc, float2 w, float2 z) {
   acc = __ffma2_rn(z, make_float2(w.x, w.x), acc);
   acc = __ffma2_rn(make_float2(z.y, z.x), make_float2(w.y, -w.y), acc);
 }
+// FFMA2 forms of the three solver updates: the operand reused across the unrolled
+// loop is the packed one (or its LO_HI swap), the other is broadcast; per component the
+// same two fmaf in the same order as the scalar forms below (bit-identical).
+// acc -= a * conj(b), a packed (L[i][j] over rows), b broadcast (L[l][j])
+__device__ __forceinline__ void cmsub_conjb2(float2& acc, float2 a, float2 b) {
+  acc = __ffma2_rn(a, make_float2(-b.x, -b.x), acc);
+  acc = __ffma2_rn(make_float2(a.y, a.x), make_float2(-b.y, b.y), acc);
+}
+// acc -= a * b, b packed (y_j[k]), a broadcast (L[i][j])
+__device__ __forceinline__ void cmsub2(float2& acc, float2 a, float2 b) {
+  acc = __ffma2_rn(b, make_float2(-a.x, -a.x), acc);
+  acc = __ffma2_rn(make_float2(b.y, b.x), make_float2(a.y, -a.y), acc);
+}
+// acc -= conj(a) * b, b packed (v_i[k]), a broadcast (L[i][m])
+__device__ __forceinline__ void cmsub_conja2(float2& acc, float2 a, float2 b) {
+  acc = __ffma2_rn(b, make_float2(-a.x, -a.x), acc);
+  acc = __ffma2_rn(make_float2(b.y, b.x), make_float2(-a.y, a.y), acc);
+}
 // acc -= a * b
 __device__ __forceinline__ void cmsub(float2& acc, float2 a, float2 b) {
   acc.x = fmaf(-a.x, b.x, acc.x);

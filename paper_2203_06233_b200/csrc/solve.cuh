@@ -134,18 +134,18 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       // they are updated unconditionally (no per-element predicate).
       if (q > qq) {
 #pragma unroll
-        for (int u = CF::umin(v); u < MR; ++u) cmsub_conjb(A[u][v], Li[u], Ll[v]);
+        for (int u = CF::umin(v); u < MR; ++u) cmsub_conjb2(A[u][v], Li[u], Ll[v]);
       }
 #pragma unroll
       for (int v2 = v + 1; v2 < MC; ++v2) {
 #pragma unroll
-        for (int u = CF::umin(v2); u < MR; ++u) cmsub_conjb(A[u][v2], Li[u], Ll[v2]);
+        for (int u = CF::umin(v2); u < MR; ++u) cmsub_conjb2(A[u][v2], Li[u], Ll[v2]);
       }
 #pragma unroll
       for (int u = CF::umin(v); u < MR; ++u) {
         if (PR * u + p > j) {  // finalised rows <= j keep y
 #pragma unroll
-          for (int kv = 0; kv < SC; ++kv) cmsub(B[u][kv], Li[u], yk[kv]);
+          for (int kv = 0; kv < SC; ++kv) cmsub2(B[u][kv], Li[u], yk[kv]);
         }
       }
     }
@@ -216,12 +216,12 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       for (int u = 0; u < ui; ++u) {  // rows m = PR*u + p < i
         const float2 lim = sh.row[PR * u + p];
 #pragma unroll
-        for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[u][kv], lim, vk[kv]);
+        for (int kv = 0; kv < SC; ++kv) cmsub_conja2(B[u][kv], lim, vk[kv]);
       }
       if (p < pi) {
         const float2 lim = sh.row[PR * ui + p];
 #pragma unroll
-        for (int kv = 0; kv < SC; ++kv) cmsub_conja(B[ui][kv], lim, vk[kv]);
+        for (int kv = 0; kv < SC; ++kv) cmsub_conja2(B[ui][kv], lim, vk[kv]);
       }
       group_sync<G>(bar_id);
     }
