@@ -83,10 +83,10 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
 #pragma unroll
     for (int m = 0; m + 1 < i; m += 2) {
       const float4 l2 = *reinterpret_cast<const float4*>(&sh.L[i][m]);
-      cmsub(Y[i], make_float2(l2.x, l2.y), Y[m]);
-      cmsub(e, make_float2(l2.z, l2.w), Y[m + 1]);
+      cmsub2(Y[i], make_float2(l2.x, l2.y), Y[m]);
+      cmsub2(e, make_float2(l2.z, l2.w), Y[m + 1]);
     }
-    if (i & 1) cmsub(Y[i], sh.L[i][i - 1], Y[i - 1]);
+    if (i & 1) cmsub2(Y[i], sh.L[i][i - 1], Y[i - 1]);
     Y[i].x = (Y[i].x + e.x) * sh.rd[i];
     Y[i].y = (Y[i].y + e.y) * sh.rd[i];
     asm volatile("" ::: "memory");  // keep each row's loads next to their use (register pressure)
@@ -103,16 +103,16 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
     // v_i -= sum_{m>i} U[i][m] v_m, row i of U read as pairs
     float2 e = make_float2(0.f, 0.f);
     if ((i + 1) & 1) {
-      if (i + 1 < N) cmsub(Y[i], sh.U[i][i + 1], Y[i + 1]);
+      if (i + 1 < N) cmsub2(Y[i], sh.U[i][i + 1], Y[i + 1]);
     }
 #pragma unroll
     for (int m = ((i + 2) & ~1); m + 1 < N; m += 2) {
       const float4 u2 = *reinterpret_cast<const float4*>(&sh.U[i][m]);
-      cmsub(Y[i], make_float2(u2.x, u2.y), Y[m]);
-      cmsub(e, make_float2(u2.z, u2.w), Y[m + 1]);
+      cmsub2(Y[i], make_float2(u2.x, u2.y), Y[m]);
+      cmsub2(e, make_float2(u2.z, u2.w), Y[m + 1]);
     }
     if ((N - ((i + 2) & ~1)) & 1) {
-      if (N - 1 > i) cmsub(Y[i], sh.U[i][N - 1], Y[N - 1]);
+      if (N - 1 > i) cmsub2(Y[i], sh.U[i][N - 1], Y[N - 1]);
     }
     Y[i].x = (Y[i].x + e.x) * sh.rd[i];
     Y[i].y = (Y[i].y + e.y) * sh.rd[i];
