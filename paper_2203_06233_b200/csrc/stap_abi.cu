@@ -355,14 +355,14 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   }
 
   // K4: fused single-kernel path when it fits and the caller's path allows it.  AUTO
-  // prefers staged when the tensor-core apply applies (medium, 16 cubes: staged 2.68 ms
-  // vs fused 3.30 ms per step on B200).
+  // takes it whenever it fits (medium, 16 cubes on B200: fused 2.48 ms vs staged 2.56 ms
+  // per step with the tcgen05 apply); shapes it cannot hold (large) run staged.
   const bool fits = fused_configure(kp, &pl->fcfg);
   if (p->path == STAP_PATH_FUSED && !fits) {
     delete pl;
     return STAP_ERR_UNSUPPORTED;
   }
-  pl->fused = (fits && (p->path == STAP_PATH_FUSED || (p->path == STAP_PATH_AUTO && !pl->apply_tc))) ? 1 : 0;
+  pl->fused = (fits && p->path != STAP_PATH_STAGED) ? 1 : 0;
 
   // staged workspace
   const long long NN = (long long)N * N;

@@ -204,7 +204,8 @@ def test_path_fused_unsupported(stap):
         plan_for(stap, cfg, path="fused")
     assert e.value.code == 3
     assert plan_for(stap, cfg).description.startswith("staged")
-    assert plan_for(stap, synth.CONFIGS["medium"]).description.startswith("staged")  # tensor-core apply
+    assert plan_for(stap, synth.CONFIGS["medium"]).description.startswith("fused")
+    assert "tcgen05" in plan_for(stap, synth.CONFIGS["medium"], path="staged").description
     assert plan_for(stap, synth.CONFIGS["small"]).description.startswith("fused")
 
 
