@@ -88,10 +88,11 @@ typedef struct {
     int32_t path;            /* stap_run's kernel path, a stap_path value (0 = auto)       */
 } stap_params;
 
-/* stap_run path.  AUTO picks the measured-faster one: the fused kernel when the shape
- * fits it (small, medium), else the staged path (large; its apply runs on the tensor
- * cores when S = 16, K % 64 == 0, N <= 64).  FUSED on a shape the fused kernel cannot
- * hold is STAP_ERR_UNSUPPORTED.  The stage entry points are independent of this field. */
+/* stap_run path.  AUTO picks the measured-faster one: the staged path when both its
+ * tensor-core stages apply (covariance: 24 <= N <= 64, K % 16 == 0; apply: S = 16,
+ * K % 64 == 0, N <= 64 -- medium, large), else the fused kernel when the shape fits it
+ * (small), else staged.  FUSED on a shape the fused kernel cannot hold is
+ * STAP_ERR_UNSUPPORTED.  The stage entry points are independent of this field. */
 typedef enum { STAP_PATH_AUTO = 0, STAP_PATH_FUSED = 1, STAP_PATH_STAGED = 2 } stap_path;
 
 /* Buffer shapes (complex64 unless noted), with B = R/K, N = C*T, Dl = dop_count:

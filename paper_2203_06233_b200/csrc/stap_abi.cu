@@ -16,6 +16,7 @@
 #include "apply.cuh"
 #include "apply_tc.cuh"
 #include "cov.cuh"
+#include "cov_tc.cuh"
 #include "fused.cuh"
 #include "solve.cuh"
 #include "solve_small.cuh"
@@ -29,6 +30,9 @@ struct stap_plan {
   // K1
   int cov_P, cov_threads, cov_runs;
   size_t cov_smem;
+  int cov_tc, cov_tc_grid, cov_tc_tiles;  // tcgen05 3xTF32 covariance (cov_tc.cuh) when supported
+  CovTcGeom cov_tc_geom;
+  size_t cov_tc_smem;
   // K2
   SolveSel solve_sel;
   int solve_small, solve_lanes;  // N <= 16: solve_small.cuh with `solve_lanes` lanes per matrix
@@ -92,6 +96,34 @@ cudaError_t set_cov_attr(int C, size_t smem) {
   return cudaGetLastError();
 }
 
+// cuTensorMapEncodeTiled from the driver, without linking libcuda
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// the cube as a 2-D fp32 tensor [batch*nbins*C rows][2R floats] with box {bx floats, by rows}
+bool encode_cube_map(const KParams& k, const float2* cube, CUtensorMap* map, int bx, int by,
+                     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE) {
+  const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * k.R, (cuuint64_t)k.batch * k.nbins * k.C};
+  const cuuint64_t strides[1] = {(cuuint64_t)k.R * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by}, estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(cube), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+
+
 template <int C>
 void cov_launch_t(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
   dim3 grid(pl->cov_runs, pl->kp.B, pl->kp.batch);
@@ -99,6 +131,13 @@ void cov_launch_t(const stap_plan* pl, const float2* cube, float2* cov, cudaStre
 }
 
 void cov_launch(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
+  CUtensorMap msw;
+  if (pl->cov_tc &&  // (an unaligned cube view takes the SIMT kernel)
+      encode_cube_map(pl->kp, cube, &msw, 32, pl->cov_tc_geom.MB * pl->kp.C, CU_TENSOR_MAP_SWIZZLE_128B)) {
+    cov_tc_kernel<<<pl->cov_tc_grid, kCovTcThreads, pl->cov_tc_smem, st>>>(msw, pl->kp, cube, cov, pl->cov_tc_tiles,
+                                                                           pl->cov_tc_geom);
+    return;
+  }
   switch (pl->kp.C) {
     case 1: cov_launch_t<1>(pl, cube, cov, st); break;
     case 2: cov_launch_t<2>(pl, cube, cov, st); break;
@@ -115,32 +154,6 @@ template <int SMAX>
 void apply_launch_t(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
   apply_kernel<SMAX><<<pl->apply_grid, pl->apply_upc * pl->apply_tpu, pl->apply_smem, st>>>(
       pl->kp, cube, w, out, pl->apply_tpu, pl->apply_upc, pl->units);
-}
-
-// cuTensorMapEncodeTiled from the driver, without linking libcuda
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }();
-  return fn;
-}
-
-// the cube as a 2-D fp32 tensor [batch*nbins*C rows][2R floats], box {128 floats, C rows}
-bool encode_cube_map(const stap_plan* pl, const float2* cube, CUtensorMap* map) {
-  const PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
-  if (!enc) return false;
-  const KParams& k = pl->kp;
-  const cuuint64_t dims[2] = {(cuuint64_t)2 * k.R, (cuuint64_t)k.batch * k.nbins * k.C};
-  const cuuint64_t strides[1] = {(cuuint64_t)k.R * 8};
-  const cuuint32_t box[2] = {128, (cuuint32_t)k.C}, estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(cube), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int KS>
@@ -163,7 +176,7 @@ void apply_tc_attr(int N, size_t smem) {
 
 void apply_launch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
   CUtensorMap map;
-  if (pl->apply_tc && encode_cube_map(pl, cube, &map)) {  // (an unaligned cube view takes the SIMT kernel)
+  if (pl->apply_tc && encode_cube_map(pl->kp, cube, &map, 128, pl->kp.C)) {  // (an unaligned cube view takes the SIMT kernel)
     switch ((pl->kp.N + 7) / 8) {
       case 1: apply_tc_launch_t<1>(pl, map, w, out, st); break;
       case 2: apply_tc_launch_t<2>(pl, map, w, out, st); break;
@@ -236,6 +249,13 @@ stap_status staged_run(const stap_plan* pl, const float2* cube, const float2* st
 extern "C" {
 
 int32_t stap_abi_version(void) { return STAP_ABI_VERSION; }
+
+#ifdef COVTC_PROF
+extern "C" int stap_debug_covtc_prof(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, stapk::g_covtc_prof, sizeof(unsigned long long) * 8);
+}
+#endif
 
 const char* stap_status_string(stap_status s) {
   switch (s) {
@@ -311,6 +331,19 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   pl->cov_threads = (cov_tpb(C) * cov_blocks(T, P + T - 1) + 31) / 32 * 32;
   pl->cov_runs = (p->dop_count + P - 1) / P;
   pl->cov_smem = cov_smem_bytes(C, T, K, P);
+  {
+    const char* e = getenv("STAP_COV_SIMT");  // developer A/B knob
+    pl->cov_tc_geom = cov_tc_geom(C, T, N, p->dop_count);
+    pl->cov_tc_tiles = p->batch * kp.B * pl->cov_tc_geom.ntd;
+    pl->cov_tc_smem = cov_tc_smem(N, pl->cov_tc_geom.RS, pl->cov_tc_geom.OB).total;
+    pl->cov_tc = (cov_tc_supported(C, T, N, K) && tensor_map_encoder() && pl->cov_tc_smem <= kSmemCap &&
+                  !(e && atoi(e)))
+                     ? 1
+                     : 0;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+    pl->cov_tc_grid = pl->cov_tc_tiles < nsm ? pl->cov_tc_tiles : nsm;  // persistent, one CTA per SM
+  }
 
   // K2: lane-group layout for (N, S); 256 threads per CTA
   if (!solve_select(N, S, &pl->solve_sel)) {
@@ -355,14 +388,16 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   }
 
   // K4: fused single-kernel path when it fits and the caller's path allows it.  AUTO
-  // takes it whenever it fits (medium, 16 cubes on B200: fused 2.48 ms vs staged 2.56 ms
-  // per step with the tcgen05 apply); shapes it cannot hold (large) run staged.
+  // prefers the staged path when both tensor-core stages apply (K1 and K3 on tcgen05;
+  // medium, 16 cubes on B200: staged 2.30 ms vs fused 2.48 ms per step), else the fused
+  // kernel when it fits (small); shapes it cannot hold (large) run staged.
   const bool fits = fused_configure(kp, &pl->fcfg);
   if (p->path == STAP_PATH_FUSED && !fits) {
     delete pl;
     return STAP_ERR_UNSUPPORTED;
   }
-  pl->fused = (fits && p->path != STAP_PATH_STAGED) ? 1 : 0;
+  const bool tc_staged = pl->cov_tc && pl->apply_tc;
+  pl->fused = (fits && (p->path == STAP_PATH_FUSED || (p->path == STAP_PATH_AUTO && !tc_staged))) ? 1 : 0;
 
   // staged workspace
   const long long NN = (long long)N * N;
@@ -381,7 +416,9 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
       delete pl;
       return STAP_ERR_DEVICE;
     }
-    if (set_cov_attr(C, pl->cov_smem) != cudaSuccess) {
+    if (set_cov_attr(C, pl->cov_smem) != cudaSuccess ||
+        (pl->cov_tc && cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)pl->cov_tc_smem) != cudaSuccess)) {
       delete pl;
       cudaGetLastError();
       return STAP_ERR_CUDA;
@@ -402,8 +439,8 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
   if (pl->fused)
     snprintf(pl->desc, sizeof pl->desc, "fused:%s", pl->fcfg.name);
   else
-    snprintf(pl->desc, sizeof pl->desc, "staged:cov(P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(%s,tpu=%d,upc=%d)",
-             pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
+    snprintf(pl->desc, sizeof pl->desc, "staged:cov(%s,P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(%s,tpu=%d,upc=%d)",
+             pl->cov_tc ? "tcgen05-3xtf32" : "simt", pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
              pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
              pl->apply_upc);
   *out_plan = pl;

@@ -127,6 +127,35 @@ def test_covariance_vs_oracle(stap, name):
     assert np.all(np.diagonal(cov, axis1=-2, axis2=-1).imag == 0)
 
 
+def test_covariance_large_tc_vs_oracle(stap):
+    """The tcgen05 covariance at the large shape (N = 56), on a D that has wrapped edge tiles."""
+    cfg = synth.CONFIGS["large"].with_(D=40, R=1024)
+    cube = synth.datacube(cfg)
+    Rref, _ = oracle.covariance(OP(cfg), cube)
+    plan = plan_for(stap, cfg, path="staged")
+    assert "cov(tcgen05" in plan.description
+    cov = plan.covariance(dev(cube).reshape(plan.cube_shape)).cpu().numpy()[0]
+    num = np.linalg.norm((cov - Rref).reshape(cfg.D, cfg.B, -1), axis=-1)
+    den = np.linalg.norm(Rref.reshape(cfg.D, cfg.B, -1), axis=-1)
+    assert (num / den).max() <= 1e-5
+    assert np.array_equal(cov, np.conj(np.swapaxes(cov, -1, -2)))
+    assert np.all(np.diagonal(cov, axis1=-2, axis2=-1).imag == 0)
+
+
+@pytest.mark.parametrize("name", ["small", "medium"])
+def test_covariance_batch_bitwise(stap, name):
+    """A batched covariance equals each cube's own (every tile of every cube, incl. wrapped ones)."""
+    cfg = synth.CONFIGS[name]
+    M = 6
+    xs = np.stack([synth.datacube(cfg, i) for i in range(M)])
+    pb = plan_for(stap, cfg, batch=M, path="staged")
+    p1 = plan_for(stap, cfg, path="staged")
+    cb = pb.covariance(dev(xs).reshape(pb.cube_shape)).cpu().numpy()
+    for n in range(M):
+        c1 = p1.covariance(dev(xs[n:n + 1]).reshape(p1.cube_shape)).cpu().numpy()[0]
+        assert np.array_equal(cb[n], c1), n
+
+
 @pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
 def test_solve_vs_oracle(stap, name):
     """K2 fed the GPU's own complex64 covariance; the oracle solves the same bytes."""
@@ -204,8 +233,9 @@ def test_path_fused_unsupported(stap):
         plan_for(stap, cfg, path="fused")
     assert e.value.code == 3
     assert plan_for(stap, cfg).description.startswith("staged")
-    assert plan_for(stap, synth.CONFIGS["medium"]).description.startswith("fused")
-    assert "tcgen05" in plan_for(stap, synth.CONFIGS["medium"], path="staged").description
+    dm = plan_for(stap, synth.CONFIGS["medium"]).description
+    assert dm.startswith("staged") and "cov(tcgen05" in dm and "apply(tcgen05" in dm
+    assert plan_for(stap, synth.CONFIGS["medium"], path="fused").description.startswith("fused")
     assert plan_for(stap, synth.CONFIGS["small"]).description.startswith("fused")
 
 
@@ -217,10 +247,22 @@ def test_fused_equals_staged(stap, name):
     st = synth.steering(cfg, "ula")
     pf, Yf, If = run_gpu(stap, cfg, cube, st, path="fused")
     assert pf.description.startswith("fused")
-    res = run_gpu(stap, cfg, cube, st, staged=True)
+    # same arithmetic: the staged path with the SIMT covariance (K1's developer knob)
+    os.environ["STAP_COV_SIMT"] = "1"
+    try:
+        res = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
+    finally:
+        del os.environ["STAP_COV_SIMT"]
+    assert "cov(simt" in res[0].description
     assert np.array_equal(If, res[2])
     e = rel_lines(Yf, res[1]).max()
     assert e <= 1e-5, e
+    # the default staged path (tcgen05 3xTF32 covariance where it applies) agrees within
+    # the oracle tolerance: R differs by <= ~2e-6 relative, amplified at most by the
+    # loaded condition number (<= N / lambda)
+    res2 = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
+    assert np.array_equal(If, res2[2])
+    assert rel_lines(Yf, res2[1]).max() <= 1e-3
 
 
 @pytest.mark.parametrize("name,G", [("tiny", 3), ("small", 2), ("small", 8), ("medium", 4)])
