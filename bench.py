@@ -280,6 +280,8 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        # NCCL's version banner goes to stdout; the contract is one JSON line there
+        os.environ["NCCL_DEBUG"] = os.environ.get("STAP_NCCL_DEBUG", "WARN")
         dist.init_process_group("nccl", device_id=dev)
 
     gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes)
