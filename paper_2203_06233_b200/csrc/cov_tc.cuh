@@ -46,7 +46,7 @@ __device__ unsigned long long g_covtc_prof[8];  // [6] = tiles; [7] = band copy 
 #endif
 
 constexpr int kCovTcCompute = 4;  // compute warps: TMEM lanes 0..127
-constexpr int kCovTcWriter = 4;   // writer warps: R_d assembly and stores, overlapped with the next tile
+constexpr int kCovTcWriter = 8;   // writer warps: R_d assembly and stores, overlapped with the next tile
 constexpr int kCovTcThreads = (kCovTcCompute + kCovTcWriter) * 32 + 64;  // + producer warp + MMA warp
 #ifndef COVTC_STAGES
 #define COVTC_STAGES 2
