@@ -11,9 +11,9 @@
 //   reduction i = snapshot element t*C + c, zero-padded to 8*KS         -> K = 8 per MMA
 //   Out[m][n] = sum_i A[m][i] B[n][i],  A[2jj+p][i] = part_p(z_i[jj]),  B as above
 //   Re Y[k][jj] = Out[2jj][k] + Out[2jj+1][S+k],  Im Y[k][jj] = Out[2jj+1][k] - Out[2jj][S+k]
-// 3xTF32: x = hi + lo, hi = x rounded to TF32, lo = x - hi (exact; |lo| <= 2^-12 |x|, the
-//   tensor core truncates it to TF32, error <= 2^-23 |x|);
-//   A B ~= Ahi Bhi + Ahi Blo + Alo Bhi (the dropped Alo Blo is <= 2^-24 |A||B|),
+// 3xTF32: x = hi + lo with hi = x as stored (the tensor core reads it truncated to TF32)
+//   and lo = x - trunc_TF32(x) (exact, |lo| < 2^-10 |x|, truncated by the MMA in turn:
+//   error < 2^-21 |x|);  A B ~= Ahi Bhi + Ahi Blo + Alo Bhi (dropped Alo Blo < 2^-20 |A||B|),
 //   FP32 accumulation in tensor memory.
 //
 // Data movement (B200-first):
@@ -49,7 +49,11 @@ constexpr int kApplyTcSmemBudget = 112 * 1024;  // two CTAs per SM
 // barriers.  A stage holds the N snapshot rows of a tile (512 B
 // each) and, for a unit's first tile, its S x N weights.
 __host__ __device__ inline uint32_t apply_tc_b_bytes(int KS) { return (uint32_t)KS * 2048u; }
-__host__ __device__ inline uint32_t apply_tc_stage_bytes(int N) { return (uint32_t)N * (512u + 16u * 8u); }
+// a stage: NP = 8*ceil(N/8) snapshot rows of 512 B (rows N..NP-1 stay zero: the A loads
+// need no bounds test) then the unit's S x N weights
+__host__ __device__ inline uint32_t apply_tc_stage_bytes(int N) {
+  return (uint32_t)((N + 7) & ~7) * 512u + (uint32_t)N * 16u * 8u;
+}
 __host__ inline int apply_tc_stages(int N) {
   const int KS = (N + 7) / 8;
   const int ns = (int)((kApplyTcSmemBudget - apply_tc_b_bytes(KS) - 512) / apply_tc_stage_bytes(N));
@@ -99,6 +103,9 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
     mbar_init(mma_bar, 1);
     fence_mbar_init();
   }
+  for (int s = 0; s < ns; ++s)  // snapshot rows N..NP-1 of every stage: zero, never written by TMA
+    for (int i = tid; i < (NP - N) * 128; i += blockDim.x)
+      reinterpret_cast<float*>(stage0 + (size_t)s * stage_bytes + (size_t)N * 512)[i] = 0.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
         const int base = local_bin(p, d - p.h);  // local row of bin d-h; the window wraps mod D
         unsigned char* dst = stage0 + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&full[s], (uint32_t)N * 512u + (t.mt == 0 ? wbytes : 0u));
-        if (t.mt == 0) bulk_g2s(dst + (size_t)N * 512, wts + (long long)t.u * S * N, wbytes, &full[s]);
+        if (t.mt == 0) bulk_g2s(dst + (size_t)NP * 512, wts + (long long)t.u * S * N, wbytes, &full[s]);
         const int x = 2 * (t.b * K + t.mt * 64), y0 = n * p.nbins * C;
         for (int tt = 0; tt < p.T; ++tt) {
           int lb = base + tt;
@@ -196,11 +203,10 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
         for (int pp = 0; pp < 2; ++pp) {
           const int nn = pp * S + k;
           const float x = pp ? w.y : w.x;
-          const float hi = tf32_hi(x);
           const uint32_t off =
               (uint32_t)(i >> 3) * 2048u + (nn >> 3) * 256 + ((i >> 2) & 1) * 128 + (nn & 7) * 16 + (i & 3) * 4;
-          *reinterpret_cast<float*>(bb + off) = hi;
-          *reinterpret_cast<float*>(bb + off + 4 * 256) = x - hi;  // row nn + 32
+          *reinterpret_cast<float*>(bb + off) = x;                                // hi (truncated by the MMA)
+          *reinterpret_cast<float*>(bb + off + 4 * 256) = x - tf32_trunc(x);     // lo, row nn + 32
         }
       }
     };
@@ -209,13 +215,15 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
       float a[8], b[8], c[8], d[8];
       const uint32_t acc = tmem + lane_base + 128 + 64 * par + 8 * hq;
       tmem_ld8x4(acc, acc + S, acc + 32, acc + 32 + S, a, b, c, d);
-      float* yf =
-          reinterpret_cast<float*>(out + (long long)x.nd * S * R + (long long)x.b * K + x.mt * 64 + jj) + part;
+      float* yp = reinterpret_cast<float*>(out + (long long)x.nd * S * R + (long long)(8 * hq) * R +
+                                           (long long)x.b * K + x.mt * 64 + jj) + part;
+      const float sg = part ? -1.f : 1.f;  // Re: own + partner; Im: own - partner
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float re = a[k] + c[k];                                  // Out[m][k]
         const float o = __shfl_xor_sync(0xffffffffu, b[k] + d[k], 1);  // partner row's Out[.][S+k]
-        yf[(long long)(8 * hq + k) * R * 2] = part ? (re - o) : (re + o);  // Re: own+partner; Im: own-partner
+        *yp = fmaf(sg, o, re);
+        yp += 2 * R;
       }
     };
 
@@ -227,18 +235,17 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
       mbar_wait(&full[s], ph);
       float z[KH][8];
 #pragma unroll
-      for (int kh = 0; kh < KH; ++kh)
+      for (int kh = 0; kh < KH; ++kh) {
+        const float* zk = zs + (hq + 2 * kh) * 8 * 128;  // rows 8ks .. 8ks+7 (padding rows are zero)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int i = 8 * (hq + 2 * kh) + e;
-          z[kh][e] = (i < N && hq + 2 * kh < KS) ? zs[i * 128] : 0.f;
-        }
+        for (int e = 0; e < 8; ++e) z[kh][e] = (hq + 2 * kh < KS) ? zk[e * 128] : 0.f;
+      }
       if (j >= 1) {  // MMA(j-1) done: A, B and accumulator (j-1) & 1 are ready
         mbar_wait(mma_bar, (uint32_t)(j - 1) & 1u);
         tc_fence_after();
       }
       if (t.mt == 0) {
-        stage_b(reinterpret_cast<const float2*>(stage0 + (size_t)s * stage_bytes + (size_t)N * 512), bbuf);
+        stage_b(reinterpret_cast<const float2*>(stage0 + (size_t)s * stage_bytes + (size_t)NP * 512), bbuf);
         fence_proxy_async();  // generic-proxy B stores -> visible to the tensor core
       }
       // A: row m, k-steps hq + 2kh: hi at column 8ks, lo at 64 + 8ks
@@ -246,13 +253,10 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
       for (int kh = 0; kh < KH; ++kh) {
         const int ks = hq + 2 * kh;
         if (ks < KS) {
-          float h[8], l[8];
+          float l[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            h[e] = tf32_hi(z[kh][e]);
-            l[e] = z[kh][e] - h[e];
-          }
-          tmem_st8(tmem + lane_base + 8 * ks, h);
+          for (int e = 0; e < 8; ++e) l[e] = z[kh][e] - tf32_trunc(z[kh][e]);
+          tmem_st8(tmem + lane_base + 8 * ks, z[kh]);  // hi: the tensor core truncates to TF32
           tmem_st8(tmem + lane_base + 64 + 8 * ks, l);
         }
       }

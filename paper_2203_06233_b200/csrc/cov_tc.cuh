@@ -311,10 +311,6 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
           ih[e] = tf32_hi(imv[e]);
           il[e] = imv[e] - ih[e];
         }
-        // release the stage only after the loaded values have been USED: an mbarrier
-        // arrive does not wait for this thread's outstanding shared loads, so an arrive
-        // right after issuing them lets the next TMA overwrite the row mid-read (seen)
-        mbar_arrive(&empty[s]);
         COVTC_T(w2);
         if (cc >= 2) {  // MMAs of chunk cc-2 done: A buffer pb and B planes pb are free
           mbar_wait(&mma_done[pb], (uint32_t)((cc - 2) >> 1) & 1u);
@@ -331,6 +327,12 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
         tmem_st8(ab + 40, rl + 8);
         tmem_st8(ab + 48, il);
         tmem_st8(ab + 56, il + 8);
+        // release the stage only here: the tcgen05.st above consume (as asm operands) values
+        // derived from every loaded element, so the shared loads have completed.  An
+        // mbarrier arrive does not wait for outstanding loads, and the compiler may sink
+        // plain arithmetic below an arrive, so an earlier release let the next TMA
+        // overwrite a row mid-read (seen as run-to-run differences in one Gram row/column)
+        mbar_arrive(&empty[s]);
         // B planes, K-major core matrices: (row m, cell k) at (k/8)*4096 + (m/8)*256 +
         // ((k/4)%2)*128 + (m%8)*16 + (k%4)*4 -- four cells per 16-byte store
         unsigned char* bp = bpl + (size_t)pb * kCovTcBBytes + (m >> 3) * 256 + (m & 7) * 16;

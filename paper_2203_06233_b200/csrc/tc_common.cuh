@@ -134,6 +134,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// x truncated to TF32 (the value the tensor core reads from an fp32 operand)
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 // round x to TF32 (10-bit mantissa, ties away from zero) with integer ops: adding half
 // a TF32 ulp to the magnitude bits and truncating; the low 13 bits are 0
 __device__ __forceinline__ float tf32_hi(float x) {

@@ -247,19 +247,21 @@ def test_fused_equals_staged(stap, name):
     st = synth.steering(cfg, "ula")
     pf, Yf, If = run_gpu(stap, cfg, cube, st, path="fused")
     assert pf.description.startswith("fused")
-    # same arithmetic: the staged path with the SIMT covariance (K1's developer knob)
+    # same arithmetic: the staged path with the SIMT covariance and apply (developer knobs)
     os.environ["STAP_COV_SIMT"] = "1"
+    os.environ["STAP_APPLY_SIMT"] = "1"
     try:
         res = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
     finally:
         del os.environ["STAP_COV_SIMT"]
-    assert "cov(simt" in res[0].description
+        del os.environ["STAP_APPLY_SIMT"]
+    assert "cov(simt" in res[0].description and "apply(simt" in res[0].description
     assert np.array_equal(If, res[2])
     e = rel_lines(Yf, res[1]).max()
     assert e <= 1e-5, e
-    # the default staged path (tcgen05 3xTF32 covariance where it applies) agrees within
-    # the oracle tolerance: R differs by <= ~2e-6 relative, amplified at most by the
-    # loaded condition number (<= N / lambda)
+    # the default staged path (tcgen05 3xTF32 covariance and apply where they apply) agrees
+    # within the oracle tolerance: R differs by <= ~2e-6 relative, amplified at most by
+    # the loaded condition number (<= N / lambda); the apply adds <= ~1e-6 per line
     res2 = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
     assert np.array_equal(If, res2[2])
     assert rel_lines(Yf, res2[1]).max() <= 1e-3
@@ -393,9 +395,12 @@ def test_repeat_runs_bitwise(stap, name):
         c = plan.covariance(dc)
         w, g, j = plan.solve_weights(c, ds)
         a = plan.apply(dc, w)
-        assert torch.equal(y, y0) and torch.equal(i, i0)
-        assert torch.equal(c, c0) and torch.equal(w, w0) and torch.equal(g, g0) and torch.equal(j, j0)
-        assert torch.equal(a, a0)
+        assert torch.equal(c, c0), "covariance"
+        assert torch.equal(w, w0) and torch.equal(g, g0) and torch.equal(j, j0), "solve"
+        assert torch.equal(a, a0), "apply"
+        assert torch.equal(i, i0), "run info"
+        assert torch.equal(y, y0), "run"
+
 
 
 def test_wrap_only_window_shard(stap):
