@@ -128,9 +128,13 @@ stap_status stap_run(const stap_plan* plan, const stap_c64* cube, const stap_c64
                      stap_c64* out, int32_t* info, void* workspace, size_t workspace_bytes,
                      cudaStream_t stream);
 /* Whole path from HOST buffers (pinned for async copies): enqueues H2D of cube and
- * steering, stap_run, and D2H of out and info, all on `stream`; the caller
- * synchronises the stream before reading h_out / h_info.  Device staging lives
- * in `workspace` (>= stap_plan_workspace_bytes(plan, 1, .)). */
+ * steering, the kernels, and D2H of out and info; the caller synchronises `stream`
+ * before reading h_out / h_info (the call makes `stream` wait for everything it
+ * enqueued).  For batch >= 2 the plan pipelines the batch in up to 8 chunks of whole
+ * cubes on two internal streams (H2D of chunk c+1 and D2H of chunk c-1 overlap the
+ * kernels of chunk c; PCIe moves both directions at once); calls on one plan must
+ * therefore come from one host thread at a time.  Device staging lives in
+ * `workspace` (>= stap_plan_workspace_bytes(plan, 1, .)). */
 stap_status stap_run_host(const stap_plan* plan, const stap_c64* h_cube, const stap_c64* h_steering,
                           stap_c64* h_out, int32_t* h_info, void* workspace, size_t workspace_bytes,
                           cudaStream_t stream);

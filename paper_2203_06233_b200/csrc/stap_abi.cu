@@ -50,7 +50,27 @@ struct stap_plan {
   size_t ws_cov, ws_w, ws_g, ws_total;
   size_t cube_bytes, steer_bytes, out_bytes, info_bytes;
   char desc[160];
+  // stap_run_host pipelining: the batch in io_nch chunks run by a child plan (batch / io_nch),
+  // host->device copies, kernels and device->host copies of different chunks overlapped
+  stap_plan* io_child = nullptr;
+  int io_nch = 0;
+  cudaStream_t io_s[2] = {nullptr, nullptr};
+  cudaEvent_t io_ev[2 + 2 * 8] = {};
 };
+
+namespace {
+void plan_free(stap_plan* pl) {
+  if (!pl) return;
+  if (pl->io_nch) {
+    for (cudaEvent_t& e : pl->io_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t& q : pl->io_s)
+      if (q) cudaStreamDestroy(q);
+  }
+  plan_free(pl->io_child);
+  delete pl;
+}
+}  // namespace
 
 namespace {
 
@@ -270,7 +290,11 @@ const char* stap_status_string(stap_status s) {
   return "STAP_ERR_UNKNOWN";
 }
 
-stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
+static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, bool with_io);
+
+stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) { return plan_create_impl(p, out_plan, true); }
+
+static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, bool with_io) {
   if (!p || !out_plan) return STAP_ERR_NULL_ARG;
   *out_plan = nullptr;
   const int C = p->n_chan, T = p->tdof, D = p->n_dop, R = p->n_range, K = p->training_block,
@@ -443,12 +467,37 @@ stap_status stap_plan_create(const stap_params* p, stap_plan** out_plan) {
              pl->cov_tc ? "tcgen05-3xtf32" : "simt", pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
              pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
              pl->apply_upc);
+  // host-I/O pipelining (stap_run_host): up to 8 equal chunks of whole cubes
+  const int M = p->batch;
+  const int nch = (M % 8 == 0) ? 8 : (M % 4 == 0) ? 4 : (M % 2 == 0) ? 2 : 1;
+  if (with_io && nch > 1) {
+    stap_params cp = *p;
+    cp.batch = M / nch;
+    stap_plan* child = nullptr;
+    bool ok = plan_create_impl(&cp, &child, false) == STAP_OK && child->info_bytes % 16 == 0 &&
+              child->cube_bytes % 16 == 0 && child->out_bytes % 16 == 0;
+    if (ok) {
+      DeviceGuard g(p->device);
+      pl->io_child = child;
+      pl->io_nch = nch;
+      ok = g.ok;
+      for (cudaStream_t& q : pl->io_s) ok = ok && cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) == cudaSuccess;
+      for (cudaEvent_t& e : pl->io_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    } else {
+      plan_free(child);
+    }
+    if (!ok) {
+      plan_free(pl);
+      cudaGetLastError();
+      return STAP_ERR_CUDA;
+    }
+  }
   *out_plan = pl;
   return STAP_OK;
 }
 
 stap_status stap_plan_destroy(stap_plan* plan) {
-  delete plan;
+  plan_free(plan);
   return STAP_OK;
 }
 
@@ -530,6 +579,40 @@ stap_status stap_run_host(const stap_plan* pl, const stap_c64* h_cube, const sta
   char* d_steer = d_cube + align_up(pl->cube_bytes, 256);
   char* d_out = d_steer + align_up(pl->steer_bytes, 256);
   char* d_info = d_out + align_up(pl->out_bytes, 256);
+  if (pl->io_nch) {
+    // chunk c: H2D on io_s[0] -> kernels on `st` -> D2H on io_s[1]; PCIe runs both directions
+    // at once, so the D2H of chunk c overlaps the H2D of chunk c+1 and the kernels
+    const stap_plan* ch = pl->io_child;
+    cudaStream_t sin = pl->io_s[0], sout = pl->io_s[1];
+    cudaEvent_t e_entry = pl->io_ev[0], e_exit = pl->io_ev[1];
+    const cudaEvent_t* e_in = pl->io_ev + 2;
+    const cudaEvent_t* e_done = pl->io_ev + 2 + pl->io_nch;
+    bool ok = cudaEventRecord(e_entry, st) == cudaSuccess && cudaStreamWaitEvent(sin, e_entry, 0) == cudaSuccess &&
+              cudaStreamWaitEvent(sout, e_entry, 0) == cudaSuccess &&
+              cudaMemcpyAsync(d_steer, h_steering, pl->steer_bytes, cudaMemcpyHostToDevice, sin) == cudaSuccess;
+    for (int c = 0; ok && c < pl->io_nch; ++c) {
+      ok = cudaMemcpyAsync(d_cube + c * ch->cube_bytes, reinterpret_cast<const char*>(h_cube) + c * ch->cube_bytes,
+                           ch->cube_bytes, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+           cudaEventRecord(e_in[c], sin) == cudaSuccess;
+    }
+    for (int c = 0; ok && c < pl->io_nch; ++c) {
+      ok = cudaStreamWaitEvent(st, e_in[c], 0) == cudaSuccess &&
+           stap_run(ch, reinterpret_cast<const stap_c64*>(d_cube + c * ch->cube_bytes),
+                    reinterpret_cast<const stap_c64*>(d_steer), reinterpret_cast<stap_c64*>(d_out + c * ch->out_bytes),
+                    reinterpret_cast<int32_t*>(d_info + c * ch->info_bytes), workspace, ch->ws_total, st) == STAP_OK &&
+           cudaEventRecord(e_done[c], st) == cudaSuccess && cudaStreamWaitEvent(sout, e_done[c], 0) == cudaSuccess &&
+           cudaMemcpyAsync(reinterpret_cast<char*>(h_out) + c * ch->out_bytes, d_out + c * ch->out_bytes, ch->out_bytes,
+                           cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+           cudaMemcpyAsync(reinterpret_cast<char*>(h_info) + c * ch->info_bytes, d_info + c * ch->info_bytes,
+                           ch->info_bytes, cudaMemcpyDeviceToHost, sout) == cudaSuccess;
+    }
+    ok = ok && cudaEventRecord(e_exit, sout) == cudaSuccess && cudaStreamWaitEvent(st, e_exit, 0) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      return STAP_ERR_CUDA;
+    }
+    return STAP_OK;
+  }
   if (cudaMemcpyAsync(d_cube, h_cube, pl->cube_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(d_steer, h_steering, pl->steer_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return check_launch() == STAP_OK ? STAP_ERR_CUDA : STAP_ERR_CUDA;

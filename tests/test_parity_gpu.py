@@ -325,6 +325,27 @@ def test_run_host_matches_device(stap):
     assert np.array_equal(ho.numpy(), Yd) and np.array_equal(hi.numpy(), Id)
 
 
+@pytest.mark.parametrize("name,M", [("small", 8), ("medium", 4), ("large", 2)])
+def test_run_host_pipelined_batch(stap, name, M):
+    """Batched stap_run_host (chunked, copies overlapped on internal streams) == device stap_run."""
+    cfg = synth.CONFIGS[name]
+    if name != "small":
+        cfg = cfg.with_(D=32)
+    xs = np.stack([synth.datacube(cfg, i) for i in range(M)])
+    st = synth.steering(cfg, "ula")
+    plan = plan_for(stap, cfg, batch=M)
+    yd, idv = plan.run(dev(xs).reshape(plan.cube_shape), dev(st))
+    hc = torch.from_numpy(xs).pin_memory()
+    hs = torch.from_numpy(st).pin_memory()
+    ho = torch.full(plan.out_shape, float("nan"), dtype=torch.complex64).pin_memory()
+    hi = torch.full(plan.info_shape, -7, dtype=torch.int32).pin_memory()
+    ws = torch.empty(plan.host_workspace_bytes, dtype=torch.uint8, device="cuda:0")
+    for _ in range(2):  # twice: the second call must order after the first
+        plan.run_host(hc, hs, ho, hi, ws)
+        torch.cuda.synchronize()
+        assert np.array_equal(ho.numpy(), yd.cpu().numpy()) and np.array_equal(hi.numpy(), idv.cpu().numpy())
+
+
 # ---------------------------------------------------------------- edge and degenerate cases
 @pytest.mark.parametrize("kw", [
     dict(C=1, T=1, D=1, R=8, K=2, S=1),        # N = 1, D = T = 1
