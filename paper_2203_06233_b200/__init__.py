@@ -189,10 +189,11 @@ class StapPlan:
         self.description = stap_plan_describe(self.handle)
         self._ws = None
 
-    def __del__(self):
+    def __del__(self, _destroy=_lib.stap_plan_destroy, _vp=_vp):
+        # the defaults keep the C function reachable during interpreter shutdown
         h = getattr(self, "handle", None)
         if h:
-            _lib.stap_plan_destroy(_vp(h))
+            _destroy(_vp(h))
             self.handle = None
 
     # shapes ------------------------------------------------------------
