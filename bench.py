@@ -280,9 +280,20 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        # NCCL's version banner goes to stdout; the contract is one JSON line there
+        # NCCL prints a version banner on stdout when the first communicator is built; the
+        # contract is one JSON line there, so fd 1 points at stderr until that has happened
         os.environ["NCCL_DEBUG"] = os.environ.get("STAP_NCCL_DEBUG", "WARN")
-        dist.init_process_group("nccl", device_id=dev)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier(device_ids=[local_rank])
+            torch.cuda.synchronize(dev)
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
 
     gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes)
     M = args.cubes
