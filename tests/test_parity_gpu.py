@@ -142,6 +142,25 @@ def test_covariance_large_tc_vs_oracle(stap):
     assert np.all(np.diagonal(cov, axis1=-2, axis2=-1).imag == 0)
 
 
+@pytest.mark.parametrize("name", ["medium", "large"])
+@pytest.mark.parametrize("lam", [1e-2, 1e-3])
+def test_tensor_core_path_vs_oracle_lambda(stap, name, lam):
+    """SURVEY 8(f) NEXT-4 pin: the 3xTF32 tcgen05 covariance + apply path (staged) against
+    the fp64 oracle at lambda = 1e-2 and 1e-3 (a lighter loading amplifies the R error)."""
+    cfg = synth.CONFIGS[name].with_(D=24, lam=lam)
+    if name == "large":
+        cfg = cfg.with_(R=1024)
+    cube = synth.datacube(cfg)
+    st = synth.steering(cfg, "ula")
+    plan = plan_for(stap, cfg, path="staged")
+    assert "cov(tcgen05" in plan.description and "apply(tcgen05" in plan.description
+    ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
+    y, info = plan.run(dev(cube).reshape(plan.cube_shape), dev(st))
+    Y, I = y.cpu().numpy()[0], info.cpu().numpy()[0]
+    assert np.array_equal(I, ref["info"])
+    assert rel_lines(Y, ref["Y"]).max() <= 1e-3
+
+
 @pytest.mark.parametrize("name", ["small", "medium"])
 def test_covariance_batch_bitwise(stap, name):
     """A batched covariance equals each cube's own (every tile of every cube, incl. wrapped ones)."""
