@@ -95,11 +95,13 @@ def _load():
             lib.stap_oracle_solve_f64.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, vp, vp, vp, vp, vp]
             lib.stap_oracle_cholesky_f64.argtypes = [ctypes.c_int32, vp, vp]
             lib.stap_oracle_apply.argtypes = [P, vp, vp, vp]
+            lib.stap_oracle_doppler.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                vp, vp, vp, ctypes.c_int32]
             lib.stap_oracle_run.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int32]
             lib.stap_oracle_gj_inverse.argtypes = [ctypes.c_int32, vp, vp]
             for f in ("stap_oracle_covariance", "stap_oracle_solve", "stap_oracle_solve_f64",
                       "stap_oracle_cholesky_f64", "stap_oracle_apply", "stap_oracle_run",
-                      "stap_oracle_gj_inverse", "stap_oracle_max_threads"):
+                      "stap_oracle_gj_inverse", "stap_oracle_max_threads", "stap_oracle_doppler"):
                 getattr(lib, f).restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -208,3 +210,19 @@ def gj_inverse(A) -> np.ndarray:
     if rc:
         raise np.linalg.LinAlgError("singular")
     return Ainv
+
+
+def doppler(window, raw, nthreads: int = 1) -> np.ndarray:
+    """Doppler front end: X[n][d][c][r] = sum_p w[p] x[n][p][c][r] exp(-2 pi i p d / D), from
+    complex64 raw [batch][D][C][R] (a 3-D array is one cube) and float32 window [D]; complex128 out."""
+    raw = _c64(raw)
+    one = raw.ndim == 3
+    if one:
+        raw = raw[None]
+    n, D, C, R = raw.shape
+    w = np.ascontiguousarray(window, np.float32)
+    if w.shape != (D,):
+        raise ValueError("window must have D entries")
+    out = np.zeros(raw.shape, np.complex128)
+    _check(_load().stap_oracle_doppler(D, C, R, n, _ptr(w), _ptr(raw), _ptr(out), int(nthreads)), "doppler")
+    return out[0] if one else out

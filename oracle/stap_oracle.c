@@ -439,6 +439,58 @@ int stap_oracle_gj_inverse(int32_t n, const double* A, double* Ainv) {
     return 0;
 }
 
+/*
+ * Doppler front end (reading c-19 in DESIGN.md): the per-row
+ * taper and FFT along the pulse axis that turn raw pulses into the datacube
+ * (Table 2 "fft_2D,axis=1"; Fig. 7 text):
+ *   X[d][c][r] = sum_{p < D} w[p] x[p][c][r] exp(-2 pi i p d / D)
+ * written out as the DFT definition: a sequential fp64 sum in ascending p, the phase
+ * taken from (p*d mod D) exactly.  raw [batch][D][C][R] complex64 (interleaved
+ * floats), window [D] float, out [batch][D][C][R] complex128 (interleaved doubles).
+ * The paper's following 2-D x 2-D multiply (its "U") is ambiguous and not modelled.
+ */
+int stap_oracle_doppler(int32_t D, int32_t C, int32_t R, int32_t batch, const float* window, const float* raw,
+                        double* out, int32_t nthreads) {
+    if (D <= 0 || C <= 0 || R <= 0 || batch <= 0 || !window || !raw || !out) return OR_BAD;
+    double* ct = (double*)malloc(sizeof(double) * (size_t)D);
+    double* st = (double*)malloc(sizeof(double) * (size_t)D);
+    if (!ct || !st) {
+        free(ct);
+        free(st);
+        return OR_NOMEM;
+    }
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t k = 0; k < D; ++k) {  /* exp(-2 pi i k / D) = cos - i sin */
+        ct[k] = cos(two_pi * (double)k / (double)D);
+        st[k] = -sin(two_pi * (double)k / (double)D);
+    }
+    const int64_t plane = (int64_t)C * R;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1) collapse(2)
+#endif
+    for (int64_t n = 0; n < batch; ++n) {
+        for (int64_t col = 0; col < plane; ++col) {
+            const float* xr = raw + 2 * (n * D * plane + col);
+            double* xo = out + 2 * (n * D * plane + col);
+            for (int64_t d = 0; d < D; ++d) {
+                double re = 0.0, im = 0.0;
+                for (int64_t q = 0; q < D; ++q) {
+                    const double a = (double)window[q] * (double)xr[2 * q * plane];
+                    const double bim = (double)window[q] * (double)xr[2 * q * plane + 1];
+                    const int64_t k = (q * d) % D;
+                    re += a * ct[k] - bim * st[k];
+                    im += a * st[k] + bim * ct[k];
+                }
+                xo[2 * d * plane] = re;
+                xo[2 * d * plane + 1] = im;
+            }
+        }
+    }
+    free(ct);
+    free(st);
+    return OR_OK;
+}
+
 int stap_oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -474,3 +474,55 @@ def test_generator_statistics():
     x = synth.cn(123, 0, np.arange(200000))
     assert abs(np.mean(np.abs(x) ** 2) - 1) < 0.01
     assert abs(np.mean(x)) < 0.01
+
+
+# ---------------------------------------------------------------- Doppler front end
+def _raw(D, C, R, seed=0, n=None):
+    rng = np.random.default_rng(seed)
+    shape = (D, C, R) if n is None else (n, D, C, R)
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64)
+
+
+def test_doppler_is_the_dft_numpy():
+    """Special case reducing to a library routine: the windowed DFT along pulses = numpy.fft.fft."""
+    D, C, R = 16, 3, 5
+    x = _raw(D, C, R)
+    w = np.hanning(D).astype(np.float32)
+    X = oracle.doppler(w, x)
+    ref = np.fft.fft(w.astype(np.float64)[:, None, None] * x.astype(np.complex128), axis=0)
+    assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_doppler_parseval():
+    D, C, R = 32, 2, 4
+    x = _raw(D, C, R, seed=1)
+    w = (0.5 + np.arange(D) / D).astype(np.float32)
+    X = oracle.doppler(w, x)
+    wx = w.astype(np.float64)[:, None, None] * x.astype(np.complex128)
+    assert abs(np.sum(np.abs(X) ** 2) - D * np.sum(np.abs(wx) ** 2)) <= 1e-12 * D * np.sum(np.abs(wx) ** 2)
+
+
+def test_doppler_tone_lands_in_its_bin():
+    """x[p] = exp(+2 pi i f p / D), w = 1  ->  X[d] = D delta(d - f)  (sign convention of the transform)."""
+    D, f = 64, 5
+    p = np.arange(D)
+    x = np.exp(2j * np.pi * f * p / D).astype(np.complex64)[:, None, None] * np.ones((1, 2, 3), np.complex64)
+    X = oracle.doppler(np.ones(D, np.float32), x)
+    expect = np.zeros(D)
+    expect[f] = D
+    assert np.abs(X[:, 1, 2] - expect).max() <= 1e-5 * D  # complex64 input rounding of the tone
+
+
+def test_doppler_shift_theorem_and_batch():
+    """A one-pulse circular delay multiplies bin d by exp(-2 pi i d / D); batched = per cube."""
+    D, C, R = 16, 2, 3
+    x = _raw(D, C, R, seed=2)
+    w = np.ones(D, np.float32)
+    X0 = oracle.doppler(w, x)
+    X1 = oracle.doppler(w, np.roll(x, 1, axis=0))
+    ramp = np.exp(-2j * np.pi * np.arange(D) / D)[:, None, None]
+    assert np.abs(X1 - ramp * X0).max() <= 1e-12 * np.abs(X0).max()
+    xb = _raw(D, C, R, seed=3, n=3)
+    Xb = oracle.doppler(w, xb)
+    for n in range(3):
+        assert np.array_equal(Xb[n], oracle.doppler(w, xb[n]))
