@@ -468,6 +468,24 @@ def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=1
         r = roofline_obj(c[name]["flops"] * M, c[name]["bytes"] * M, t, pk)
         res[name] = {"us": t * 1e6, "bound": r["bound"], "achieved": r["achieved"], "unit": r["unit"],
                      "frac": r["frac"]}
+    # the front end (not part of the step): stap_doppler on a cube-shaped
+    # input, HBM-bound (one read, one write of the cube)
+    D = plan.dims.D
+    if plan.dop_count == D and plan.cube_bins == D and D >= 2 and (D & (D - 1)) == 0 and D <= 8192:
+        win = torch.ones(D, dtype=torch.float32, device=cube.device)
+        dcube = torch.empty_like(cube)
+        plan.doppler(cube, win, dcube, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            plan.doppler(cube, win, dcube, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / reps
+        nbytes = 2.0 * cube.numel() * 8
+        res["doppler_front_end"] = {"us": t * 1e6, "bound": "hbm", "achieved": nbytes / t / 1e9, "unit": "GB/s",
+                                    "frac": nbytes / t / 1e9 / pk["hbm_gbs"], "note": "not in the step (NEXT-3)"}
     return res
 
 

@@ -116,6 +116,15 @@ const char* stap_plan_describe(const stap_plan* plan);
 /* Stage 1: loaded covariance of every owned unit.  Reads only the bins each window needs. */
 stap_status stap_covariance(const stap_plan* plan, const stap_c64* cube, stap_c64* cov,
                             cudaStream_t stream);
+/* Front end (DESIGN reading c-19): the datacube from raw pulses,
+ *   cube[n][d][c][r] = sum_{p < D} window[p] raw[n][p][c][r] exp(-2 pi i p d / D),
+ * the per-row taper and FFT along the pulse axis (Table 2 "fft_2D,axis=1").
+ * raw and cube: [batch][D][C][R] complex64 (device, 16-byte aligned, distinct);
+ * window: D floats (device).  Needs a plan over the whole cube (dop_begin = 0,
+ * dop_count = cube_bins = n_dop, cube_bin0 = 0) and D a power of two, 2 <= D <= 8192:
+ * otherwise STAP_ERR_UNSUPPORTED. */
+stap_status stap_doppler(const stap_plan* plan, const float* window, const stap_c64* raw, stap_c64* cube,
+                         cudaStream_t stream);
 /* Stage 2: Cholesky + forward/back solves -> MVDR weights, gamma, info. */
 stap_status stap_solve_weights(const stap_plan* plan, const stap_c64* cov, const stap_c64* steering,
                                stap_c64* weights, float* gamma, int32_t* info, cudaStream_t stream);

@@ -31,7 +31,7 @@ STATUS = {0: "STAP_OK", 1: "STAP_ERR_NULL_ARG", 2: "STAP_ERR_BAD_DIMS", 3: "STAP
           4: "STAP_ERR_MISALIGNED", 5: "STAP_ERR_CUDA", 7: "STAP_ERR_DEVICE"}
 
 SYMBOLS = ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_plan_describe",
-           "stap_covariance", "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host",
+           "stap_doppler", "stap_covariance", "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host",
            "stap_status_string", "stap_abi_version")
 
 
@@ -63,6 +63,7 @@ _lib.stap_plan_workspace_bytes.argtypes = [_vp, ctypes.c_int32, ctypes.POINTER(c
 _lib.stap_plan_describe.argtypes = [_vp]
 _lib.stap_plan_describe.restype = ctypes.c_char_p
 _lib.stap_covariance.argtypes = [_vp, _vp, _vp, _vp]
+_lib.stap_doppler.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.stap_solve_weights.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.stap_apply.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.stap_run.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
@@ -70,7 +71,7 @@ _lib.stap_run_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _v
 _lib.stap_status_string.argtypes = [ctypes.c_int]
 _lib.stap_status_string.restype = ctypes.c_char_p
 _lib.stap_abi_version.restype = ctypes.c_int32
-for _f in ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_covariance",
+for _f in ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_doppler", "stap_covariance",
            "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host"):
     getattr(_lib, _f).restype = ctypes.c_int
 
@@ -122,6 +123,10 @@ def stap_plan_workspace_bytes(plan: int, host_io: bool = False) -> int:
 
 def stap_plan_describe(plan: int) -> str:
     return _lib.stap_plan_describe(_vp(plan)).decode()
+
+
+def stap_doppler(plan: int, window, raw, cube, stream) -> None:
+    _check(_lib.stap_doppler(_vp(plan), _ptr(window), _ptr(raw), _ptr(cube), stream), "stap_doppler")
 
 
 def stap_covariance(plan: int, cube, cov, stream) -> None:
@@ -231,6 +236,18 @@ class StapPlan:
             raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
 
     # stages ------------------------------------------------------------
+    def doppler(self, raw, window, cube=None, stream=None):
+        """The datacube from raw pulses [batch][D][C][R] (stap_doppler): taper + FFT along pulses."""
+        import torch
+        self._chk(raw, self.cube_shape, torch.complex64, "raw")
+        if window.dtype != torch.float32 or window.shape != (self.dims.D,) or window.device != raw.device:
+            raise ValueError("window: float32 [D] on the cube's device")
+        if cube is None:
+            cube = torch.empty(self.cube_shape, dtype=torch.complex64, device=raw.device)
+        self._chk(cube, self.cube_shape, torch.complex64, "cube")
+        stap_doppler(self.handle, window.contiguous(), raw, cube, _stream(stream, self.device))
+        return cube
+
     def covariance(self, cube, cov=None, stream=None):
         import torch
         self._chk(cube, self.cube_shape, torch.complex64, "cube")

@@ -1,0 +1,83 @@
+// doppler.cuh -- K0, the Doppler front end (reading c-19):
+//   X[d][c][r] = sum_{p < D} w[p] x[p][c][r] exp(-2 pi i p d / D)
+// the per-row taper and FFT along the pulse axis that turn raw pulses into the datacube
+// (Table 2 "fft_2D,axis=1"; Fig. 7 text).
+//
+// B200 design: HBM-bound (one read and one write of the cube; the FFT's 5 D log2 D flops
+// per column are far below the ridge).  A CTA takes RC consecutive range cells of one
+// channel of one cube -- every pulse row of that tile is one contiguous RC*8-byte
+// piece, so loads and stores are coalesced -- keeps the D x RC tile in shared memory,
+// and runs an in-place radix-2 decimation-in-time FFT on every column: the taper is
+// applied at the load, which also scatters rows to bit-reversed positions; log2(D)
+// butterfly stages follow, threads over (butterfly, cell) with the cell index fastest
+// so a warp touches consecutive words of one or two rows (bank-conflict free).
+// Twiddles exp(-2 pi i k / D), k < D/2, come from sincospif into shared memory once per
+// CTA.  D must be a power of two (2 .. 8192).
+#pragma once
+#include "common.cuh"
+
+namespace stapk {
+
+constexpr int kDopplerThreads = 256;
+constexpr size_t kDopplerTileBytes = 48 * 1024;  // four CTAs per SM
+
+// cells per CTA: the largest power of two <= 64 that divides R and keeps D*RC*8 + the
+// twiddles within kDopplerTileBytes
+__host__ inline int doppler_rc(int D, int R) {
+  int rc = 64;
+  while (rc > 1 && ((size_t)D * rc * 8 + (size_t)D / 2 * 8 > kDopplerTileBytes || R % rc)) rc >>= 1;
+  return rc;
+}
+__host__ inline size_t doppler_smem(int D, int rc) { return (size_t)D * rc * 8 + (size_t)(D / 2) * 8; }
+
+__device__ __forceinline__ int bitrev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
+
+__global__ void __launch_bounds__(kDopplerThreads, 4)
+    doppler_kernel(const float2* __restrict__ raw, const float* __restrict__ window, float2* __restrict__ out,
+                   int D, int logD, int C, int R, int lrc) {
+  const int rc = 1 << lrc, jm = rc - 1;
+  extern __shared__ __align__(16) float2 dsm[];
+  float2* tile = dsm;           // [D][rc]
+  float2* tw = dsm + D * rc;    // [D/2]
+  const int r0 = blockIdx.x * rc, c = blockIdx.y, n = blockIdx.z;
+  const long long plane = (long long)C * R;
+  const float2* src = raw + (long long)n * D * plane + (long long)c * R + r0;
+  float2* dst = out + (long long)n * D * plane + (long long)c * R + r0;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < D / 2; k += blockDim.x) {
+    float s, co;
+    sincospif(-2.0f * (float)k / (float)D, &s, &co);
+    tw[k] = make_float2(co, s);
+  }
+  // load + taper, rows to bit-reversed positions
+#pragma unroll 4
+  for (int idx = tid; idx < D * rc; idx += blockDim.x) {
+    const int p = idx >> lrc, j = idx & jm;
+    const float2 v = __ldg(src + (long long)p * plane + j);
+    const float w = __ldg(window + p);
+    tile[(bitrev(p, logD) << lrc) + j] = make_float2(v.x * w, v.y * w);
+  }
+  __syncthreads();
+  // radix-2 DIT stages: span 2h, twiddle exp(-2 pi i pos / 2h) = tw[pos * D / 2h]
+  for (int s = 0; s < logD; ++s) {
+    const int h = 1 << s, tstride = D >> (s + 1);
+#pragma unroll 2
+    for (int b = tid; b < (D / 2) * rc; b += blockDim.x) {
+      const int k = b >> lrc, j = b & jm;
+      const int pos = k & (h - 1), i0 = ((k >> s) << (s + 1)) + pos, i1 = i0 + h;
+      const float2 t = tw[pos * tstride];
+      const float2 a = tile[(i0 << lrc) + j], u = tile[(i1 << lrc) + j];
+      const float2 bu = make_float2(fmaf(u.x, t.x, -u.y * t.y), fmaf(u.x, t.y, u.y * t.x));
+      tile[(i0 << lrc) + j] = make_float2(a.x + bu.x, a.y + bu.y);
+      tile[(i1 << lrc) + j] = make_float2(a.x - bu.x, a.y - bu.y);
+    }
+    __syncthreads();
+  }
+#pragma unroll 4
+  for (int idx = tid; idx < D * rc; idx += blockDim.x) {
+    const int d = idx >> lrc, j = idx & jm;
+    dst[(long long)d * plane + j] = tile[idx];
+  }
+}
+
+}  // namespace stapk

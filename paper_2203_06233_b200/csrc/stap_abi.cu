@@ -17,6 +17,7 @@
 #include "apply_tc.cuh"
 #include "cov.cuh"
 #include "cov_tc.cuh"
+#include "doppler.cuh"
 #include "fused.cuh"
 #include "solve.cuh"
 #include "solve_small.cuh"
@@ -512,6 +513,33 @@ stap_status stap_plan_workspace_bytes(const stap_plan* pl, int32_t host_io, size
 }
 
 const char* stap_plan_describe(const stap_plan* pl) { return pl ? pl->desc : "(null plan)"; }
+
+stap_status stap_doppler(const stap_plan* pl, const float* window, const stap_c64* raw, stap_c64* cube,
+                         cudaStream_t st) {
+  if (!pl || !window || !raw || !cube) return STAP_ERR_NULL_ARG;
+  const stap_params& p = pl->prm;
+  const int D = p.n_dop;
+  if (p.dop_begin != 0 || p.dop_count != D || p.cube_bins != D || p.cube_bin0 != 0 || D < 2 || D > 8192 ||
+      (D & (D - 1)))
+    return STAP_ERR_UNSUPPORTED;
+  if (!aligned16(raw) || !aligned16(cube) || (reinterpret_cast<uintptr_t>(window) & 3u)) return STAP_ERR_MISALIGNED;
+  DeviceGuard g(p.device);
+  if (!g.ok) return STAP_ERR_DEVICE;
+  const int rc = doppler_rc(D, p.n_range);
+  const size_t smem = doppler_smem(D, rc);
+  int logD = 0, lrc = 0;
+  while ((1 << logD) < D) ++logD;
+  while ((1 << lrc) < rc) ++lrc;
+  if (cudaFuncSetAttribute(doppler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return STAP_ERR_CUDA;
+  }
+  dim3 grid(p.n_range / rc, p.n_chan, p.batch);
+  doppler_kernel<<<grid, kDopplerThreads, smem, st>>>(reinterpret_cast<const float2*>(raw), window,
+                                                      reinterpret_cast<float2*>(cube), D, logD, p.n_chan,
+                                                      p.n_range, lrc);
+  return check_launch();
+}
 
 stap_status stap_covariance(const stap_plan* pl, const stap_c64* cube, stap_c64* cov, cudaStream_t st) {
   if (!pl || !cube || !cov) return STAP_ERR_NULL_ARG;

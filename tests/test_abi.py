@@ -81,6 +81,7 @@ def test_null_args(pkg):
     assert pkg._lib.stap_plan_create(ctypes.byref(_params(pkg)), None) == 1
     assert pkg._lib.stap_run(None, None, None, None, None, None, 0, None) == 1
     assert pkg._lib.stap_covariance(None, None, None, None) == 1
+    assert pkg._lib.stap_doppler(None, None, None, None, None) == 1
     assert pkg._lib.stap_plan_destroy(None) == 0
 
 

@@ -455,3 +455,55 @@ def test_wrap_only_window_shard(stap):
     local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
     _, Y, _ = run_gpu(stap, cfg, local, st, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb)
     assert np.array_equal(Y[0], Yfull[0, lo:lo + cnt])
+
+
+# ---------------------------------------------------------------- Doppler front end
+@pytest.mark.parametrize("name,kw,M", [("tiny", {}, 1), ("small", {}, 2), ("medium", dict(R=128), 1),
+                                       ("large", dict(R=128), 1), ("small", dict(D=8192, R=64, K=32), 1)])
+def test_doppler_vs_oracle(stap, name, kw, M):
+    """K0 (stap_doppler) against the fp64 windowed DFT, per (cube, channel, cell) column over d."""
+    cfg = synth.CONFIGS[name].with_(**kw)
+    rng = np.random.default_rng(7)
+    raw = (rng.standard_normal((M, cfg.D, cfg.C, cfg.R)) + 1j * rng.standard_normal((M, cfg.D, cfg.C, cfg.R))).astype(np.complex64)
+    w = np.hanning(cfg.D + 2)[1:-1].astype(np.float32)
+    plan = plan_for(stap, cfg, batch=M)
+    X = plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w)).cpu().numpy()
+    ref = oracle.doppler(w, raw, nthreads=NT)
+    err = np.linalg.norm(X - ref, axis=1) / np.linalg.norm(ref, axis=1)  # over d
+    assert err.max() <= 1e-5, err.max()
+    # deterministic
+    X2 = plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w)).cpu().numpy()
+    assert np.array_equal(X, X2)
+
+
+def test_doppler_front_end_feeds_the_path(stap):
+    """raw -> stap_doppler -> stap_run equals the oracle chain doppler -> run (within the Y tolerance)."""
+    cfg = synth.CONFIGS["small"].with_(D=64)
+    rng = np.random.default_rng(8)
+    raw = (rng.standard_normal((cfg.D, cfg.C, cfg.R)) + 1j * rng.standard_normal((cfg.D, cfg.C, cfg.R))).astype(np.complex64)
+    w = np.hanning(cfg.D + 2)[1:-1].astype(np.float32)
+    st = synth.steering(cfg, "ula")
+    plan = plan_for(stap, cfg)
+    cube = plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w))
+    y, info = plan.run(cube, dev(st))
+    ref = oracle.run(OP(cfg), plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w)).cpu().numpy()[0], st, nthreads=NT)
+    assert np.array_equal(info.cpu().numpy()[0], ref["info"])
+    assert rel_lines(y.cpu().numpy()[0], ref["Y"]).max() <= 1e-3
+
+
+def test_doppler_rejects(stap):
+    cfg = synth.CONFIGS["small"]
+    import torch
+    w = torch.ones(cfg.D, dtype=torch.float32, device="cuda")
+    b0, nb = synth.shard_window(cfg, 0, 8)
+    shard = plan_for(stap, cfg, dop_begin=0, dop_count=8, cube_bin0=b0, cube_bins=nb)
+    raw = torch.zeros(shard.cube_shape, dtype=torch.complex64, device="cuda")
+    with pytest.raises(stap.StapError) as e:
+        shard.doppler(raw, w)
+    assert e.value.code == 3
+    odd = synth.CONFIGS["small"].with_(D=48)
+    p = plan_for(stap, odd)
+    with pytest.raises(stap.StapError) as e:
+        p.doppler(torch.zeros(p.cube_shape, dtype=torch.complex64, device="cuda"),
+                  torch.ones(odd.D, dtype=torch.float32, device="cuda"))
+    assert e.value.code == 3
