@@ -8,8 +8,8 @@
 // channel of one cube -- every pulse row of that tile is one contiguous RC*8-byte
 // piece, so loads and stores are coalesced -- keeps the D x RC tile in shared memory,
 // and runs an in-place radix-2 decimation-in-time FFT on every column: the taper is
-// applied at the load, which also scatters rows to bit-reversed positions; log2(D)
-// butterfly stages follow, threads over (butterfly, cell) with the cell index fastest
+// applied at the load, which also scatters rows to bit-reversed positions; the log2(D)
+// butterfly stages follow two at a time (radix-4 passes), threads over (butterfly, cell) with the cell index fastest
 // so a warp touches consecutive words of one or two rows (bank-conflict free).
 // Twiddles exp(-2 pi i k / D), k < D/2, come from sincospif into shared memory once per
 // CTA.  D must be a power of two (2 .. 8192).
@@ -58,18 +58,46 @@ __global__ void __launch_bounds__(kDopplerThreads, 4)
     tile[(bitrev(p, logD) << lrc) + j] = make_float2(v.x * w, v.y * w);
   }
   __syncthreads();
-  // radix-2 DIT stages: span 2h, twiddle exp(-2 pi i pos / 2h) = tw[pos * D / 2h]
-  for (int s = 0; s < logD; ++s) {
-    const int h = 1 << s, tstride = D >> (s + 1);
+  // radix-2 DIT stages (span 2h, twiddle exp(-2 pi i pos / 2h) = tw[pos * D / 2h]), two at a
+  // time: a thread takes the 4 elements i0 + {0, h, 2h, 3h} of a span-4h group through
+  // stage s (pairs (i0,i1), (i2,i3), twiddle W_2h^pos) and stage s+1 (pairs (i0,i2) with
+  // W_4h^pos, (i1,i3) with W_4h^(pos+h)) in registers -- the same operations as two
+  // radix-2 passes, half the shared-memory passes and barriers
+  auto bfly = [](float2& a, float2& u, float2 t) {
+    const float2 bu = make_float2(fmaf(u.x, t.x, -u.y * t.y), fmaf(u.x, t.y, u.y * t.x));
+    u = make_float2(a.x - bu.x, a.y - bu.y);
+    a = make_float2(a.x + bu.x, a.y + bu.y);
+  };
+  int s = 0;
+  for (; s + 1 < logD; s += 2) {
+    const int h = 1 << s, t1 = D >> (s + 1), t2 = D >> (s + 2);
 #pragma unroll 2
+    for (int b = tid; b < (D / 4) * rc; b += blockDim.x) {
+      const int k = b >> lrc, j = b & jm;
+      const int pos = k & (h - 1), i0 = ((k >> s) << (s + 2)) + pos;
+      float2 x0 = tile[(i0 << lrc) + j], x1 = tile[((i0 + h) << lrc) + j];
+      float2 x2 = tile[((i0 + 2 * h) << lrc) + j], x3 = tile[((i0 + 3 * h) << lrc) + j];
+      const float2 w1 = tw[pos * t1];
+      bfly(x0, x1, w1);
+      bfly(x2, x3, w1);
+      bfly(x0, x2, tw[pos * t2]);
+      bfly(x1, x3, tw[(pos + h) * t2]);
+      tile[(i0 << lrc) + j] = x0;
+      tile[((i0 + h) << lrc) + j] = x1;
+      tile[((i0 + 2 * h) << lrc) + j] = x2;
+      tile[((i0 + 3 * h) << lrc) + j] = x3;
+    }
+    __syncthreads();
+  }
+  if (s < logD) {  // odd log2 D: one last radix-2 stage
+    const int h = 1 << s, tstride = D >> (s + 1);
     for (int b = tid; b < (D / 2) * rc; b += blockDim.x) {
       const int k = b >> lrc, j = b & jm;
-      const int pos = k & (h - 1), i0 = ((k >> s) << (s + 1)) + pos, i1 = i0 + h;
-      const float2 t = tw[pos * tstride];
-      const float2 a = tile[(i0 << lrc) + j], u = tile[(i1 << lrc) + j];
-      const float2 bu = make_float2(fmaf(u.x, t.x, -u.y * t.y), fmaf(u.x, t.y, u.y * t.x));
-      tile[(i0 << lrc) + j] = make_float2(a.x + bu.x, a.y + bu.y);
-      tile[(i1 << lrc) + j] = make_float2(a.x - bu.x, a.y - bu.y);
+      const int pos = k & (h - 1), i0 = ((k >> s) << (s + 1)) + pos;
+      float2 a = tile[(i0 << lrc) + j], u = tile[((i0 + h) << lrc) + j];
+      bfly(a, u, tw[pos * tstride]);
+      tile[(i0 << lrc) + j] = a;
+      tile[((i0 + h) << lrc) + j] = u;
     }
     __syncthreads();
   }
