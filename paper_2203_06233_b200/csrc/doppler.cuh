@@ -108,4 +108,127 @@ __global__ void __launch_bounds__(kDopplerThreads, 4)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K0b, the register path for 16 <= D <= 1024: D = L1*L2 (L1, L2 <= 32), one Cooley-Tukey
+// split (n = L2*m + q, d = k1 + L1*k2):
+//   A[q][k1] = sum_m w[L2 m + q] x[L2 m + q] W_L1^(m k1)      (L1-point DFT, registers)
+//   B[q][k1] = A[q][k1] * W_D^(q k1)                            (twiddle, to shared memory)
+//   X[k1 + L1 k2] = sum_q B[q][k1] W_L2^(q k2)                  (L2-point DFT, registers)
+// -- the same sum as the windowed DFT, regrouped.  Step 1 reads its L1 pulses straight from
+// HBM (a warp covers 32/rc pulse rows of rc*8 contiguous bytes), step 2 writes its L2 bins
+// straight to HBM; shared memory is crossed once (write + read) instead of log2(D)/2 times,
+// which is what bounded K0 (measured: 12 tile traversals per 2 HBM crossings at D = 1024).
+// In-register DFTs are radix-2 DIT with compile-time indices (bit reversal is renaming);
+// W_32^k comes from a literal table in constant memory.
+
+__constant__ float2 c_w32[16] = {
+    {1.000000000e+00f, 0.000000000e+00f},   {9.807852804e-01f, -1.950903220e-01f},
+    {9.238795325e-01f, -3.826834324e-01f},  {8.314696123e-01f, -5.555702330e-01f},
+    {7.071067812e-01f, -7.071067812e-01f},  {5.555702330e-01f, -8.314696123e-01f},
+    {3.826834324e-01f, -9.238795325e-01f},  {1.950903220e-01f, -9.807852804e-01f},
+    {0.000000000e+00f, -1.000000000e+00f},  {-1.950903220e-01f, -9.807852804e-01f},
+    {-3.826834324e-01f, -9.238795325e-01f}, {-5.555702330e-01f, -8.314696123e-01f},
+    {-7.071067812e-01f, -7.071067812e-01f}, {-8.314696123e-01f, -5.555702330e-01f},
+    {-9.238795325e-01f, -3.826834324e-01f}, {-9.807852804e-01f, -1.950903220e-01f}};
+
+template <int L>
+__host__ __device__ constexpr int brev_c(int i) {
+  int r = 0;
+  for (int b = 1; b < L; b <<= 1) r = (r << 1) | ((i & b) ? 1 : 0);
+  return r;
+}
+
+// in-place L-point DFT (exp(-2 pi i n k / L)) of v, natural order in and out
+template <int L>
+__device__ __forceinline__ void dft_reg(float2 (&v)[L]) {
+  float2 a[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) a[brev_c<L>(i)] = v[i];
+#pragma unroll
+  for (int h = 1; h < L; h <<= 1) {
+#pragma unroll
+    for (int g = 0; g < L; g += 2 * h) {
+#pragma unroll
+      for (int pos = 0; pos < h; ++pos) {
+        const float2 y = a[g + pos + h];
+        float2 t;
+        if (pos == 0) {
+          t = y;
+        } else if (2 * pos == h) {  // W_2h^(h/2) = -i
+          t = make_float2(y.y, -y.x);
+        } else {
+          const float2 w = c_w32[pos * (16 / h)];  // W_2h^pos = W_32^(pos*32/2h)
+          t = make_float2(fmaf(y.x, w.x, -y.y * w.y), fmaf(y.x, w.y, y.y * w.x));
+        }
+        const float2 x = a[g + pos];
+        a[g + pos] = make_float2(x.x + t.x, x.y + t.y);
+        a[g + pos + h] = make_float2(x.x - t.x, x.y - t.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < L; ++i) v[i] = a[i];
+}
+
+#ifndef STAP_DOPPLER2_MAX_SMEM
+#define STAP_DOPPLER2_MAX_SMEM (80 * 1024)
+#endif
+constexpr size_t kDoppler2MaxSmem = STAP_DOPPLER2_MAX_SMEM;  // rc = 16 up to D = 512, 8 at D = 1024
+
+// shared bytes: B tile [L1][L2*rc + pad] + twiddles W_D^n (n < D)
+__host__ inline int doppler2_pad(int rc) { return rc < 16 ? rc : 0; }
+__host__ inline size_t doppler2_smem(int L1, int L2, int rc) {
+  return ((size_t)L1 * (L2 * rc + doppler2_pad(rc)) + (size_t)L1 * L2) * 8;
+}
+
+template <int L1, int L2>
+__global__ void __launch_bounds__(kDopplerThreads, 2)
+    doppler2_kernel(const float2* __restrict__ raw, const float* __restrict__ window, float2* __restrict__ out,
+                    int C, int R, int lrc, int pad) {
+  constexpr int D = L1 * L2;
+  const int rc = 1 << lrc, jm = rc - 1;
+  const int ld = L2 * rc + pad;  // row stride of the B tile (pad: rc < 16 spreads step-2 rows over banks)
+  extern __shared__ __align__(16) float2 dsm[];
+  float2* tile = dsm;          // [L1][ld]: B[q][k1] at tile[k1*ld + q*rc + j]
+  float2* tw = dsm + L1 * ld;  // [D]
+  const int r0 = blockIdx.x * rc, c = blockIdx.y, n = blockIdx.z;
+  const long long plane = (long long)C * R;
+  const float2* src = raw + (long long)n * D * plane + (long long)c * R + r0;
+  float2* dst = out + (long long)n * D * plane + (long long)c * R + r0;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < D; k += kDopplerThreads) {
+    float s, co;
+    sincospif(-2.0f * (float)k / (float)D, &s, &co);
+    tw[k] = make_float2(co, s);
+  }
+  __syncthreads();
+  for (int item = tid; item < L2 * rc; item += kDopplerThreads) {
+    const int q = item >> lrc, j = item & jm;
+    float2 v[L1];
+#pragma unroll
+    for (int m = 0; m < L1; ++m) v[m] = __ldg(src + (long long)(L2 * m + q) * plane + j);
+#pragma unroll
+    for (int m = 0; m < L1; ++m) {
+      const float w = __ldg(window + L2 * m + q);
+      v[m] = make_float2(v[m].x * w, v[m].y * w);
+    }
+    dft_reg<L1>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < L1; ++k1) {
+      const float2 t = tw[q * k1];
+      tile[k1 * ld + item] = make_float2(fmaf(v[k1].x, t.x, -v[k1].y * t.y), fmaf(v[k1].x, t.y, v[k1].y * t.x));
+    }
+  }
+  __syncthreads();
+  for (int item = tid; item < L1 * rc; item += kDopplerThreads) {
+    const int k1 = item >> lrc, j = item & jm;
+    float2 v[L2];
+#pragma unroll
+    for (int q = 0; q < L2; ++q) v[q] = tile[k1 * ld + q * rc + j];
+    dft_reg<L2>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < L2; ++k2) dst[(long long)(k1 + L1 * k2) * plane + j] = v[k2];
+  }
+}
+
 }  // namespace stapk

@@ -525,6 +525,38 @@ stap_status stap_doppler(const stap_plan* pl, const float* window, const stap_c6
   if (!aligned16(raw) || !aligned16(cube) || (reinterpret_cast<uintptr_t>(window) & 3u)) return STAP_ERR_MISALIGNED;
   DeviceGuard g(p.device);
   if (!g.ok) return STAP_ERR_DEVICE;
+  if (D >= 16 && D <= 1024) {  // K0b, the two-level register FFT
+    int logD = 0;
+    while ((1 << logD) < D) ++logD;
+    const int L1 = 1 << ((logD + 1) / 2), L2 = D / L1;
+    int rc = 16;
+    while (rc > 4 && (doppler2_smem(L1, L2, rc) > kDoppler2MaxSmem || p.n_range % rc)) rc >>= 1;
+    if (p.n_range % rc == 0) {
+      int lrc = 0;
+      while ((1 << lrc) < rc) ++lrc;
+      const size_t smem = doppler2_smem(L1, L2, rc);
+      const dim3 grid(p.n_range / rc, p.n_chan, p.batch);
+      const auto* x = reinterpret_cast<const float2*>(raw);
+      auto* y = reinterpret_cast<float2*>(cube);
+      auto launch = [&](auto kern) -> stap_status {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+          cudaGetLastError();
+          return STAP_ERR_CUDA;
+        }
+        kern<<<grid, kDopplerThreads, smem, st>>>(x, window, y, p.n_chan, p.n_range, lrc, doppler2_pad(rc));
+        return check_launch();
+      };
+      switch (D) {
+        case 16: return launch(doppler2_kernel<4, 4>);
+        case 32: return launch(doppler2_kernel<8, 4>);
+        case 64: return launch(doppler2_kernel<8, 8>);
+        case 128: return launch(doppler2_kernel<16, 8>);
+        case 256: return launch(doppler2_kernel<16, 16>);
+        case 512: return launch(doppler2_kernel<32, 16>);
+        default: return launch(doppler2_kernel<32, 32>);
+      }
+    }
+  }
   const int rc = doppler_rc(D, p.n_range);
   const size_t smem = doppler_smem(D, rc);
   int logD = 0, lrc = 0;
