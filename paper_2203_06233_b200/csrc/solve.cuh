@@ -41,9 +41,11 @@ struct SolveCfg {
 // Per-group shared scratch (floats / float2), sized for the config.
 template <class CF>
 struct SolveShared {
-  float2 col[CF::PR * CF::MR];   // column j of L (rows)
-  float2 row[CF::PC * CF::MC];   // row i of L (columns), back solve
-  float2 yb[CF::SMAXC];          // y_j (forward) / v_i (backward)
+  // double-buffered by the parity of the step, so that groups of more than one warp
+  // (bar.sync) need one group barrier per step (kOneBarrier below)
+  float2 col[2][CF::PR * CF::MR];  // raw column j of the factor (rows), pivot at [j]
+  float2 row[2][CF::PC * CF::MC];  // row i of L (columns), back solve
+  float2 yb[2][CF::SMAXC];         // raw y_j (forward) / v_i (backward)
   float rdiag[CF::PR * CF::MR];  // 1 / L[j][j]
   float gpart[CF::PR][CF::SMAXC];
   float gam[CF::SMAXC];
@@ -71,6 +73,11 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
   constexpr int PR = CF::PR, PC = CF::PC, MR = CF::MR, MC = CF::MC, SC = CF::SC, G = CF::G;
   const int p = gl / PC, q = gl - (gl / PC) * PC;
   int fail = 0;
+  // Groups of more than one warp synchronise with bar.sync, whose cost dominates a step:
+  // they publish pivot, column and y_j together into parity buffers (one barrier per step,
+  // large solve 2.33 -> 2.23 ms).  Single-warp groups (__syncwarp) keep the two-barrier
+  // step, which measured faster for them (medium solve 1.22 vs 1.32 ms).
+  constexpr bool kOneBarrier = G > 32;
 
   // ---------------- Cholesky + forward solve (right-looking)
 #pragma unroll
@@ -78,57 +85,98 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
     for (int qq = 0; qq < PC; ++qq) {
       const int j = PC * v + qq;
       if (j >= N) break;  // uniform
-      const int pj = j % PR, uj = j / PR;
-      // (a) diag owner publishes the pivot
-      if (p == pj && q == qq) {
-        float x = 0.f;
+      const int pj = j % PR, uj = j / PR, bp = kOneBarrier ? (j & 1) : 0;
+      float r;
+      if constexpr (kOneBarrier) {
+        // (a) column-j owners publish the RAW column j (its diagonal entry is the pivot),
+        // row-j owners the RAW y_j; consumers scale by r = 1/sqrt(pivot) themselves.
+        // Parity buffers: a lane can only write buffer bp again (step j+2) after every
+        // lane has passed step j+1's barrier, i.e. finished reading step j's.
+        if (q == qq) {
 #pragma unroll
-        for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u)
-          if (u == uj) x = A[u][v].x;
-        sh.xj = x;
-      }
-      group_sync<G>(bar_id);
-      // (b) every lane: pivot, scale column j / finalise y_j
-      float x = sh.xj;
-      const bool ok = finite_pos(x);
-      if (!ok && !fail) fail = j + 1;
-      if (!ok) x = 1.0f;
-      const float r = rsqrtf(x);  // one MUFU on the pivot chain
-      if (gl == 0) sh.rdiag[j] = r;
-      // column j is published RAW (consumers scale by r); the owners keep it raw
-      // and scale their whole L once after the factorisation (no per-row branch here)
-      if (q == qq) {
+          for (int u = CF::umin(v); u < MR; ++u) sh.col[bp][PR * u + p] = A[u][v];
+        }
+        if (p == pj) {
 #pragma unroll
-        for (int u = CF::umin(v); u < MR; ++u) sh.col[PR * u + p] = A[u][v];
-      }
-      if (p == pj) {
+          for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u)
+            if (u == uj) {
 #pragma unroll
-        for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u) {
-          if (u == uj) {
+              for (int kv = 0; kv < SC; ++kv) sh.yb[bp][PC * kv + q] = B[u][kv];
+            }
+        }
+        group_sync<G>(bar_id);
+        // (b) every lane: pivot, 1/sqrt; row-j owners finalise y_j
+        float x = sh.col[bp][j].x;
+        const bool ok = finite_pos(x);
+        if (!ok && !fail) fail = j + 1;
+        if (!ok) x = 1.0f;
+        r = rsqrtf(x);  // one MUFU on the pivot chain
+        if (gl == 0) sh.rdiag[j] = r;
+        if (p == pj) {
 #pragma unroll
-            for (int kv = 0; kv < SC; ++kv) {
-              B[u][kv].x *= r;
-              B[u][kv].y *= r;
-              sh.yb[PC * kv + q] = B[u][kv];
+          for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u)
+            if (u == uj) {
+#pragma unroll
+              for (int kv = 0; kv < SC; ++kv) {
+                B[u][kv].x *= r;
+                B[u][kv].y *= r;
+              }
+            }
+        }
+      } else {
+        // (a) diag owner publishes the pivot
+        if (p == pj && q == qq) {
+          float x = 0.f;
+#pragma unroll
+          for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u)
+            if (u == uj) x = A[u][v].x;
+          sh.xj = x;
+        }
+        group_sync<G>(bar_id);
+        // (b) every lane: pivot, scale column j / finalise y_j
+        float x = sh.xj;
+        const bool ok = finite_pos(x);
+        if (!ok && !fail) fail = j + 1;
+        if (!ok) x = 1.0f;
+        r = rsqrtf(x);  // one MUFU on the pivot chain
+        if (gl == 0) sh.rdiag[j] = r;
+        // column j is published RAW (consumers scale by r); the owners keep it raw
+        if (q == qq) {
+#pragma unroll
+          for (int u = CF::umin(v); u < MR; ++u) sh.col[0][PR * u + p] = A[u][v];
+        }
+        if (p == pj) {
+#pragma unroll
+          for (int u = (PC * v) / PR; u <= (PC * v + PC - 1) / PR && u < MR; ++u) {
+            if (u == uj) {
+#pragma unroll
+              for (int kv = 0; kv < SC; ++kv) {
+                B[u][kv].x *= r;
+                B[u][kv].y *= r;
+                sh.yb[0][PC * kv + q] = B[u][kv];
+              }
             }
           }
         }
+        group_sync<G>(bar_id);
       }
-      group_sync<G>(bar_id);
       // (c) rank-1 update of the trailing matrix and of the right-hand sides
       float2 Li[MR], Ll[MC], yk[SC];
 #pragma unroll
       for (int u = CF::umin(v); u < MR; ++u) {
-        const float2 c = sh.col[PR * u + p];
+        const float2 c = sh.col[bp][PR * u + p];
         Li[u] = make_float2(c.x * r, c.y * r);  // L[i][j]
       }
 #pragma unroll
       for (int v2 = v; v2 < MC; ++v2) {
-        const float2 c = sh.col[PC * v2 + q];
+        const float2 c = sh.col[bp][PC * v2 + q];
         Ll[v2] = make_float2(c.x * r, c.y * r);  // L[l][j]
       }
 #pragma unroll
-      for (int kv = 0; kv < SC; ++kv) yk[kv] = sh.yb[PC * kv + q];
+      for (int kv = 0; kv < SC; ++kv) {
+        const float2 c = sh.yb[bp][PC * kv + q];
+        yk[kv] = kOneBarrier ? make_float2(c.x * r, c.y * r) : c;  // y_j[k]
+      }
       // Only lower-triangle entries right of column j must change; the others a
       // lane holds (upper triangle, rows >= N) are never read as results, so
       // they are updated unconditionally (no per-element predicate).
@@ -150,6 +198,7 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
       }
     }
   }
+  if constexpr (kOneBarrier) group_sync<G>(bar_id);  // rdiag[N-1] was written after the last step's barrier
   // deferred column scaling: L[i][l] = raw[i][l] / sqrt(pivot_l) for every held entry
   // (diagonal and upper-triangle entries become garbage: the back solve never reads them)
 #pragma unroll
@@ -194,38 +243,39 @@ __device__ __forceinline__ int group_chol_solve(int N, int S, float2 (&A)[CF::MR
 #pragma unroll
   for (int ui = MR - 1; ui >= 0; --ui) {
     for (int pi = PR - 1; pi >= 0; --pi) {
-      const int i = PR * ui + pi;
+      const int i = PR * ui + pi, bb = kOneBarrier ? (i & 1) : 0;  // parity buffers, as in the forward loop
       if (i >= N) continue;  // uniform
       if (p == pi) {
 #pragma unroll
         for (int v = 0; v < MC; ++v)
-          if (ui >= CF::umin(v)) sh.row[PC * v + q] = A[ui][v];
+          if (ui >= CF::umin(v)) sh.row[bb][PC * v + q] = A[ui][v];
         const float r = sh.rdiag[i];
 #pragma unroll
         for (int kv = 0; kv < SC; ++kv) {
           B[ui][kv].x *= r;
           B[ui][kv].y *= r;
-          sh.yb[PC * kv + q] = B[ui][kv];
+          sh.yb[bb][PC * kv + q] = B[ui][kv];
         }
       }
       group_sync<G>(bar_id);
       float2 vk[SC];
 #pragma unroll
-      for (int kv = 0; kv < SC; ++kv) vk[kv] = sh.yb[PC * kv + q];
+      for (int kv = 0; kv < SC; ++kv) vk[kv] = sh.yb[bb][PC * kv + q];
 #pragma unroll
       for (int u = 0; u < ui; ++u) {  // rows m = PR*u + p < i
-        const float2 lim = sh.row[PR * u + p];
+        const float2 lim = sh.row[bb][PR * u + p];
 #pragma unroll
         for (int kv = 0; kv < SC; ++kv) cmsub_conja2(B[u][kv], lim, vk[kv]);
       }
       if (p < pi) {
-        const float2 lim = sh.row[PR * ui + p];
+        const float2 lim = sh.row[bb][PR * ui + p];
 #pragma unroll
         for (int kv = 0; kv < SC; ++kv) cmsub_conja2(B[ui][kv], lim, vk[kv]);
       }
-      group_sync<G>(bar_id);
+      if constexpr (!kOneBarrier) group_sync<G>(bar_id);
     }
   }
+  if constexpr (kOneBarrier) group_sync<G>(bar_id);  // every lane is done reading the last row's buffers
 
   // ---------------- normalise: w_k = v_k / gamma_k; zero failed k or a failed unit
 #pragma unroll
