@@ -468,25 +468,27 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
              pl->cov_tc ? "tcgen05-3xtf32" : "simt", pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
              pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
              pl->apply_upc);
-  // host-I/O pipelining (stap_run_host): up to 8 equal chunks of whole cubes
+  // host-I/O pipelining (stap_run_host): up to 8 equal chunks of whole cubes.  A chunk count
+  // whose per-chunk buffers would not keep 16-byte offsets is skipped (e.g. an odd number of
+  // info words per chunk); with none left, stap_run_host runs unchunked.
   const int M = p->batch;
-  const int nch = (M % 8 == 0) ? 8 : (M % 4 == 0) ? 4 : (M % 2 == 0) ? 2 : 1;
-  if (with_io && nch > 1) {
+  for (int nch = 8; with_io && nch > 1 && !pl->io_nch; nch >>= 1) {
+    if (M % nch) continue;
     stap_params cp = *p;
     cp.batch = M / nch;
     stap_plan* child = nullptr;
-    bool ok = plan_create_impl(&cp, &child, false) == STAP_OK && child->info_bytes % 16 == 0 &&
-              child->cube_bytes % 16 == 0 && child->out_bytes % 16 == 0;
-    if (ok) {
-      DeviceGuard g(p->device);
-      pl->io_child = child;
-      pl->io_nch = nch;
-      ok = g.ok;
-      for (cudaStream_t& q : pl->io_s) ok = ok && cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) == cudaSuccess;
-      for (cudaEvent_t& e : pl->io_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
-    } else {
+    const bool fit = plan_create_impl(&cp, &child, false) == STAP_OK && child->info_bytes % 16 == 0 &&
+                     child->cube_bytes % 16 == 0 && child->out_bytes % 16 == 0;
+    if (!fit) {
       plan_free(child);
+      continue;
     }
+    DeviceGuard g(p->device);
+    pl->io_child = child;
+    pl->io_nch = nch;
+    bool ok = g.ok;
+    for (cudaStream_t& q : pl->io_s) ok = ok && cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) == cudaSuccess;
+    for (cudaEvent_t& e : pl->io_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
       plan_free(pl);
       cudaGetLastError();

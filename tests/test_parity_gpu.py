@@ -344,11 +344,16 @@ def test_run_host_matches_device(stap):
     assert np.array_equal(ho.numpy(), Yd) and np.array_equal(hi.numpy(), Id)
 
 
-@pytest.mark.parametrize("name,M", [("small", 8), ("medium", 4), ("large", 2)])
+@pytest.mark.parametrize("name,M", [("small", 8), ("medium", 4), ("large", 2), ("odd-info", 2), ("odd-info", 6)])
 def test_run_host_pipelined_batch(stap, name, M):
-    """Batched stap_run_host (chunked, copies overlapped on internal streams) == device stap_run."""
-    cfg = synth.CONFIGS[name]
-    if name != "small":
+    """Batched stap_run_host (chunked, copies overlapped on internal streams) == device stap_run.
+    "odd-info": one cube's info block is 24 bytes (D = 2, B = 3), so no chunk count keeps
+    16-byte chunk offsets and the call runs unchunked (plan creation once failed there)."""
+    if name == "odd-info":
+        cfg = synth.CONFIGS["tiny"].with_(D=2, R=18, K=6, C=3, T=2)
+    else:
+        cfg = synth.CONFIGS[name]
+    if name not in ("small", "odd-info"):
         cfg = cfg.with_(D=32)
     xs = np.stack([synth.datacube(cfg, i) for i in range(M)])
     st = synth.steering(cfg, "ula")
@@ -474,6 +479,23 @@ def test_doppler_vs_oracle(stap, name, kw, M):
     # deterministic
     X2 = plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w)).cpu().numpy()
     assert np.array_equal(X, X2)
+
+
+@pytest.mark.parametrize("D", [2, 4, 16, 32, 64, 128, 2048])
+@pytest.mark.parametrize("R", [48, 24, 20, 18])
+def test_doppler_every_split_and_tile(stap, D, R):
+    """Every D = L1*L2 instantiation of the register FFT (16..128 here; 256..1024 above) and
+    its tile widths RC = 16 / 8 / 4 (R = 48 / 24 / 20), plus the shared-memory fallback (R = 18:
+    no RC >= 4 divides it; D = 2, 4, 2048 are outside the register path), vs the fp64 DFT."""
+    cfg = synth.CONFIGS["tiny"].with_(D=D, R=R, C=3, T=2, K=R // 2 if R % 4 == 0 else 6)  # K even
+    rng = np.random.default_rng(D * 100 + R)
+    raw = (rng.standard_normal((2, D, cfg.C, R)) + 1j * rng.standard_normal((2, D, cfg.C, R))).astype(np.complex64)
+    w = (0.5 + rng.random(D)).astype(np.float32)
+    plan = plan_for(stap, cfg, batch=2)
+    X = plan.doppler(dev(raw).reshape(plan.cube_shape), dev(w)).cpu().numpy()
+    ref = oracle.doppler(w, raw, nthreads=NT)
+    err = np.linalg.norm(X - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert err.max() <= 1e-5, err.max()
 
 
 def test_doppler_front_end_feeds_the_path(stap):
