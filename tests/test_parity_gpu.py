@@ -378,6 +378,13 @@ def test_run_host_pipelined_batch(stap, name, M):
     dict(C=6, T=5, D=37, R=128, K=64, S=16),   # ragged bin runs
     dict(C=5, T=2, D=11, R=40, K=4, S=7),      # C without a fused specialisation -> staged path
     dict(C=2, T=4, D=9, R=32, K=16, S=5),      # even T (h = 1)
+    # tensor-core stages (cov_tc: K % 16 == 0, 24 <= N <= 64; apply_tc: S == 16, K % 64 == 0)
+    dict(C=8, T=8, D=8, R=128, K=64, S=16),    # N = 64 on both tcgen05 stages
+    dict(C=6, T=4, D=4, R=1024, K=1024, S=16), # N = 24 (smallest tc N), K = 1024 (largest), B = 1, D = T
+    dict(C=3, T=8, D=50, R=128, K=128, S=16),  # C = 3: a Gram tile of 42 bins (126 of 128 rows)
+    dict(C=7, T=9, D=13, R=192, K=64, S=16),   # odd N = 63, ragged tiles
+    dict(C=5, T=5, D=67, R=64, K=64, S=16),    # odd N = 25, prime D (wrapped edge tiles)
+    dict(C=3, T=9, D=9, R=48, K=16, S=16),     # cov_tc at K = 16, SIMT apply (K % 64 != 0)
 ])
 @pytest.mark.parametrize("staged", [False, True])
 def test_edge_shapes(stap, kw, staged):
