@@ -169,6 +169,25 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- inputs
+def peer_gather_setup(out, world, rank, dev, dist):
+    """Fused apply -> gather (the root variant of 8(e)'s collective row).
+
+    One symmetric buffer [world][*out.shape] per rank (torch symmetric memory: the same
+    allocation mapped into every peer's address space over NVLink). Rank r's kernels are
+    handed rank 0's slice r as their Y pointer, so the apply epilogue's stores travel over
+    NVLink straight into the root's buffer: no separate gather pass and no HBM re-read of Y.
+    A device-side barrier after each step orders the stores before anyone reads them.
+    Returns (the local buffer as [world][*out.shape] complex64, this rank's destination view,
+    the rendezvous handle)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+    n = out.numel() * 2  # floats per rank slice
+    buf = symm_mem.empty(world * n, dtype=torch.float32, device=dev)
+    hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
+    dst = hdl.get_buffer(0, (n,), torch.float32, rank * n).view(torch.complex64).view(out.shape)
+    return buf.view(torch.complex64).view((world,) + tuple(out.shape)), dst, hdl
+
+
 def make_inputs(cfg, n_gpus, rank, cubes, steering_kind="ula"):
     """This rank's cube buffers [cubes][D_cfg + halo][C][R] (halo only when N > 1), complex64."""
     gcfg = cfg.with_(D=cfg.D * n_gpus) if n_gpus > 1 else cfg
@@ -238,7 +257,8 @@ def config_obj(args, cfg, world):
     return {"workload": WORKLOAD_DESC.get(cfg.name, cfg.name), "C": cfg.C, "TDOF": cfg.T, "D": cfg.D, "R": cfg.R,
             "S": cfg.S, "K": cfg.K, "lambda": cfg.lam, "cubes_per_step_per_gpu": args.cubes,
             "parallelism": f"doppler-shard x{world} (weak: global D = {cfg.D}*{world})",
-            "l2": "inputs larger than L2 (no flush)", "steering": "ULA centre-bin"}
+            "l2": "inputs larger than L2 (no flush)", "steering": "ULA centre-bin",
+            **({"gather": args.gather} if args.gather and world > 1 else {})}
 
 
 # ---------------------------------------------------------------- our arm
@@ -252,7 +272,10 @@ def main():
     ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
     ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto",
                     help="stap_run path (stap_params.path); auto = the library's measured choice")
-    ap.add_argument("--gather", action="store_true", help="NCCL all-gather of outputs after each step")
+    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer"],
+                    help="gather the outputs after each step: nccl = NCCL all-gather (the default of a bare "
+                         "--gather), nccl-root = NCCL gather to rank 0, peer = the kernels store Y straight "
+                         "into rank 0's symmetric buffer over NVLink, then a device barrier (SURVEY 8(f) NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
@@ -312,8 +335,17 @@ def main():
         gam = torch.empty(plan.info_shape + (cfg.S,), dtype=torch.float32, device=dev)
     ws = plan.workspace()
     gather_buf = None
+    y_dst = out  # where the kernels store Y
+    peer = None
     if args.gather and world > 1:
-        gather_buf = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
+        if args.gather == "peer":
+            gather_buf, y_dst, peer = peer_gather_setup(out, world, rank, dev, dist)
+        elif args.gather == "nccl-root":
+            # NCCL has no complex type: gather float32 views
+            gather_buf = [torch.empty(out.numel() * 2, dtype=torch.float32, device=dev)
+                          for _ in range(world)] if rank == 0 else None
+        else:
+            gather_buf = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
     s_ = stap._stream(stream, local_rank)
 
     ev_stage = []
@@ -329,13 +361,17 @@ def main():
             stap.stap_solve_weights(plan.handle, cov, steer, wts, gam, info, s_)
             if record:
                 e[2].record(stream)
-            stap.stap_apply(plan.handle, cube, wts, out, s_)
+            stap.stap_apply(plan.handle, cube, wts, y_dst, s_)
             if record:
                 e[3].record(stream)
                 ev_stage.append(e)
         else:
-            stap.stap_run(plan.handle, cube, steer, out, info, ws, plan.workspace_bytes, s_)
-        if gather_buf is not None:
+            stap.stap_run(plan.handle, cube, steer, y_dst, info, ws, plan.workspace_bytes, s_)
+        if peer is not None:
+            peer.barrier(channel=0)  # every rank's stores into rank 0's buffer have landed
+        elif args.gather == "nccl-root" and world > 1:
+            dist.gather(out.view(torch.float32).view(-1), gather_list=gather_buf, dst=0)
+        elif gather_buf is not None:
             dist.all_gather_into_tensor(gather_buf.view(-1), out.view(-1))
 
     def barrier():
@@ -411,6 +447,20 @@ def main():
     except Exception:
         pass
 
+    gather_check = None
+    if peer is not None:
+        # the root's peer-gathered buffer must equal an NCCL all-gather of the local outputs, bitwise
+        if staged:
+            stap.stap_apply(plan.handle, cube, wts, out, s_)
+        else:
+            stap.stap_run(plan.handle, cube, steer, out, info, ws, plan.workspace_bytes, s_)
+        ref = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
+        dist.all_gather_into_tensor(ref.view(-1), out.view(-1))
+        ok = torch.tensor([1.0 if rank != 0 or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
+                           else 0.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        gather_check = "bitwise equal to ncclAllGather" if ok.item() == 1.0 else "MISMATCH vs ncclAllGather"
+
     result = {
         "metric": "STAP datacubes/sec", "value": value, "unit": "cubes/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -418,6 +468,8 @@ def main():
         "path": plan.description, "gpu_launches": launches_per_step * args.steps, "roofline": roof,
         "clocks": clocks, "info_nonzero": ninfo_bad,
     }
+    if gather_check:
+        result["gather_check"] = gather_check
 
     # per-stage roofline fractions (BASELINE.json metric: "% of HBM/FP32 roofline per stage")
     if not args.no_stages:
