@@ -169,7 +169,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- inputs
-def peer_gather_setup(out, world, rank, dev, dist):
+def peer_gather_setup(out, world, rank, dev, dist, multicast=False):
     """Fused apply -> gather (the root variant of 8(e)'s collective row).
 
     One symmetric buffer [world][*out.shape] per rank (torch symmetric memory: the same
@@ -178,13 +178,23 @@ def peer_gather_setup(out, world, rank, dev, dist):
     NVLink straight into the root's buffer: no separate gather pass and no HBM re-read of Y.
     A device-side barrier after each step orders the stores before anyone reads them.
     Returns (the local buffer as [world][*out.shape] complex64, this rank's destination view,
-    the rendezvous handle)."""
+    the rendezvous handle).
+
+    multicast: the destination is instead the buffer's NVLS multicast address + slice r
+    (an int); the plan's out_multicast makes every Y store a multimem.st, so each rank's
+    apply epilogue writes its slice into ALL ranks' buffers: an all-gather with no
+    separate pass."""
     import torch
     import torch.distributed._symmetric_memory as symm_mem
     n = out.numel() * 2  # floats per rank slice
     buf = symm_mem.empty(world * n, dtype=torch.float32, device=dev)
     hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
-    dst = hdl.get_buffer(0, (n,), torch.float32, rank * n).view(torch.complex64).view(out.shape)
+    if multicast:
+        if not getattr(hdl, "multicast_ptr", 0):
+            raise RuntimeError("--gather multimem: no NVLS multicast support on this box")
+        dst = int(hdl.multicast_ptr) + rank * n * 4
+    else:
+        dst = hdl.get_buffer(0, (n,), torch.float32, rank * n).view(torch.complex64).view(out.shape)
     return buf.view(torch.complex64).view((world,) + tuple(out.shape)), dst, hdl
 
 
@@ -272,10 +282,12 @@ def main():
     ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
     ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto",
                     help="stap_run path (stap_params.path); auto = the library's measured choice")
-    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer"],
+    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer", "multimem"],
                     help="gather the outputs after each step: nccl = NCCL all-gather (the default of a bare "
                          "--gather), nccl-root = NCCL gather to rank 0, peer = the kernels store Y straight "
-                         "into rank 0's symmetric buffer over NVLink, then a device barrier (SURVEY 8(f) NEXT-2)")
+                         "into rank 0's symmetric buffer over NVLink, then a device barrier; multimem = an all-gather "
+                         "by multimem.st from the apply epilogue into every rank's symmetric buffer (NVLS) "
+                         "(SURVEY 8(f) NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
@@ -321,8 +333,12 @@ def main():
     gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes)
     M = args.cubes
     dims = stap.Dims(cfg.C, cfg.T, gcfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
+    mc = args.gather == "multimem" and world > 1
     plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                         device=local_rank, path=args.path)
+                         device=local_rank, path=args.path, out_multicast=mc)
+    # an ordinary-store plan of the same shape for the e2e, stage and gather-check legs
+    plan_u = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
+                           device=local_rank, path=args.path) if mc else plan
     stream = torch.cuda.current_stream(dev)
     cube = torch.from_numpy(x_h).to(dev)
     steer = torch.from_numpy(st_h).to(dev)
@@ -338,8 +354,8 @@ def main():
     y_dst = out  # where the kernels store Y
     peer = None
     if args.gather and world > 1:
-        if args.gather == "peer":
-            gather_buf, y_dst, peer = peer_gather_setup(out, world, rank, dev, dist)
+        if args.gather in ("peer", "multimem"):
+            gather_buf, y_dst, peer = peer_gather_setup(out, world, rank, dev, dist, multicast=mc)
         elif args.gather == "nccl-root":
             # NCCL has no complex type: gather float32 views
             gather_buf = [torch.empty(out.numel() * 2, dtype=torch.float32, device=dev)
@@ -451,12 +467,12 @@ def main():
     if peer is not None:
         # the root's peer-gathered buffer must equal an NCCL all-gather of the local outputs, bitwise
         if staged:
-            stap.stap_apply(plan.handle, cube, wts, out, s_)
+            stap.stap_apply(plan_u.handle, cube, wts, out, s_)
         else:
-            stap.stap_run(plan.handle, cube, steer, out, info, ws, plan.workspace_bytes, s_)
+            stap.stap_run(plan_u.handle, cube, steer, out, info, ws, plan_u.workspace_bytes, s_)
         ref = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
         dist.all_gather_into_tensor(ref.view(-1), out.view(-1))
-        ok = torch.tensor([1.0 if rank != 0 or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
+        ok = torch.tensor([1.0 if (rank != 0 and not mc) or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
                            else 0.0], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         gather_check = "bitwise equal to ncclAllGather" if ok.item() == 1.0 else "MISMATCH vs ncclAllGather"
@@ -473,11 +489,11 @@ def main():
 
     # per-stage roofline fractions (BASELINE.json metric: "% of HBM/FP32 roofline per stage")
     if not args.no_stages:
-        result["stages"] = stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, local_rank)
+        result["stages"] = stage_fractions(stap, plan_u, cube, steer, cfg, M, pk, stream, local_rank)
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     if not args.no_e2e:
-        result["e2e"] = e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist)
+        result["e2e"] = e2e_measure(stap, plan_u, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, sample, _ = cpu_oracle_rate(cfg, args.cpu_budget, sample_bins=oracle_sample_bins(cfg))
@@ -490,7 +506,7 @@ def main():
         dist.destroy_process_group()
 
 
-def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
+def stage_fractions(stap, plan_u, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
     import torch
     s_ = stap._stream(stream, dev_idx)
     cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=cube.device)
@@ -541,7 +557,7 @@ def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=1
     return res
 
 
-def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
+def e2e_measure(stap, plan_u, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
     import torch
     hc = torch.from_numpy(x_h).pin_memory()
     hs = torch.from_numpy(st_h).pin_memory()

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define STAP_ABI_VERSION 2
+#define STAP_ABI_VERSION 3
 
 typedef struct { float re, im; } stap_c64;
 typedef struct stap_plan stap_plan;
@@ -86,6 +86,18 @@ typedef struct {
     int32_t batch;           /* independent cubes per call (>= 1), stored back to back     */
     int32_t device;          /* CUDA ordinal the plan launches on                          */
     int32_t path;            /* stap_run's kernel path, a stap_path value (0 = auto)       */
+    int32_t out_multicast;   /* ABI v3.  0: `out` of stap_apply / stap_run is an ordinary
+                                device pointer (own memory or a peer-mapped buffer).
+                                1: `out` is an NVLS multicast address (CUDA multicast object
+                                bound to every rank's copy of the output buffer, e.g. torch
+                                symmetric memory's multicast_ptr plus this rank's offset);
+                                every Y store is a multimem.st, so each rank's kernels write
+                                their outputs into all ranks' buffers (an all-gather inside
+                                the apply epilogue).  The caller orders
+                                the stores before reading (a cross-rank barrier after the
+                                stream's work).  stap_run_host rejects 1 (host `out`)
+                                with STAP_ERR_UNSUPPORTED; any other value is
+                                STAP_ERR_BAD_DIMS.                                         */
 } stap_params;
 
 /* stap_run path.  AUTO picks the measured-faster one: the staged path when both its

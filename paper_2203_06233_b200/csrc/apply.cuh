@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __r
 #pragma unroll
     for (int k = 0; k < SMAX; ++k)
       if (k < S)
-        *reinterpret_cast<float4*>(yb + (long long)k * p.R + j) =
-            make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y);
+        st_y(reinterpret_cast<float4*>(yb + (long long)k * p.R + j),
+             make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y), p.y_mc);
   }
 }
 

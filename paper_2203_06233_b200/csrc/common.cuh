@@ -13,7 +13,26 @@ struct KParams {
   float lam;
   int dop_begin, dop_count, bin0, nbins, batch;
   long long cube_stride;  // complex elements per cube in the batch = nbins*C*R
+  int y_mc;               // stap_params.out_multicast: Y is an NVLS multicast address
 };
+
+// Y stores.  With p.y_mc the output pointer is a multicast (NVLS) address: one
+// multimem.st writes the value into every rank's copy of the buffer over NVSwitch
+// (the all-gather happens in the store; include/stap.h out_multicast).
+__device__ __forceinline__ void st_y(float* a, float v, int mc) {
+  if (mc) asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
+  else *a = v;
+}
+__device__ __forceinline__ void st_y(float2* a, float2 v, int mc) {
+  if (mc) asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(a), "f"(v.x), "f"(v.y) : "memory");
+  else *a = v;
+}
+__device__ __forceinline__ void st_y(float4* a, float4 v, int mc) {
+  if (mc)
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w) : "memory");
+  else *a = v;
+}
 
 // Local row of the cube buffer holding global bin a (a may be outside [0, D)):
 // (a - bin0) mod D, non-negative (reading c-3, circular Doppler wrap).

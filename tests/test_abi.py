@@ -33,7 +33,7 @@ def test_header_symbols_exported(pkg):
 
 
 def test_abi_version_and_strings(pkg):
-    assert pkg.stap_abi_version() == 2
+    assert pkg.stap_abi_version() == 3
     for code in (0, 1, 2, 3, 4, 5, 7):
         assert pkg.stap_status_string(code).startswith(pkg.STATUS[code])
 
@@ -65,6 +65,7 @@ def _params(pkg, **kw):
     (dict(dop_count=0), 2), (dict(batch=0), 2), (dict(cube_bins=300), 2), (dict(cube_bin0=256), 2),
     (dict(cube_bins=10, dop_count=20), 2),                      # window does not cover the owned bins
     (dict(path=3), 2), (dict(path=-1), 2),                      # not a stap_path
+    (dict(out_multicast=2), 2), (dict(out_multicast=-1), 2),    # not 0 or 1 (ABI v3)
     (dict(n_chan=9, tdof=7), 3), (dict(n_steering=33), 3),
     (dict(training_block=7, n_range=511), 3), (dict(n_chan=8, tdof=9), 3),
 ])

@@ -1,7 +1,9 @@
 """Fused apply -> gather over NVLink peer stores (8(e) collective row).
 
 Two ranks, one GPU each: every rank's kernels store Y straight into rank 0's symmetric
-buffer (bench.py --gather peer). bench.py compares the root's buffer with an NCCL
+buffer (bench.py --gather peer), or, with multimem, every Y store is a multimem.st to the
+buffer's NVLS multicast address and lands in both ranks' buffers (--gather multimem).
+bench.py compares the gathered buffer (rank 0; every rank for multimem) with an NCCL
 all-gather of the same outputs and reports "gather_check"; the test requires bitwise equality.
 Needs two GPUs (gpurun --gpus 2); skipped on a one-GPU box.
 """
@@ -17,16 +19,36 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("gather", ["peer", "multimem"])
 @pytest.mark.parametrize("config", ["tiny", "small", "medium"])
-def test_peer_gather_bitwise_vs_nccl(config):
+def test_peer_gather_bitwise_vs_nccl(config, gather):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str({"tiny": 29611, "small": 29612, "medium": 29613}[config]),
+           "--master-addr", "127.0.0.1", "--master-port", str({"tiny": 29611, "small": 29612, "medium": 29613}[config] + (10 if gather == "multimem" else 0)),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--steps", "2", "--warmup", "3",
-           "--gather", "peer", "--no-stages", "--no-e2e", "--no-cpu-baseline"]
+           "--gather", gather, "--no-stages", "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["gather_check"] == "bitwise equal to ncclAllGather", line
     assert line["info_nonzero"] == 0
+
+
+@pytest.mark.gpu
+def test_run_host_rejects_multicast_out():
+    """A host `out` is never a multicast address: stap_run_host returns STAP_ERR_UNSUPPORTED."""
+    import paper_2203_06233_b200 as stap
+    sys.path.insert(0, ROOT)
+    import synth
+    cfg = synth.CONFIGS["tiny"]
+    dims = stap.Dims(cfg.C, cfg.T, cfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
+    plan = stap.StapPlan(dims, out_multicast=True)
+    hc = torch.zeros(plan.cube_shape, dtype=torch.complex64).pin_memory()
+    hs = torch.zeros((cfg.S, cfg.C * cfg.T), dtype=torch.complex64).pin_memory()
+    ho = torch.empty(plan.out_shape, dtype=torch.complex64).pin_memory()
+    hi = torch.empty(plan.info_shape, dtype=torch.int32).pin_memory()
+    ws = torch.empty(max(plan.host_workspace_bytes, 16), dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(stap.StapError) as e:
+        plan.run_host(hc, hs, ho, hi, ws)
+    assert e.value.code == 3
