@@ -169,7 +169,12 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- inputs
-def peer_gather_setup(out, world, rank, dev, dist, multicast=False):
+def plan_shape_out(stap, dims, lo, cnt, b0, nb, M):
+    """Y's shape for a plan of these dims (include/stap.h: [batch][Dl][S][R])."""
+    return (M, cnt, dims.S, dims.R)
+
+
+def peer_gather_setup(out, world, rank, dev, dist, mode="peer"):
     """Fused apply -> gather (the root variant of 8(e)'s collective row).
 
     One symmetric buffer [world][*out.shape] per rank (torch symmetric memory: the same
@@ -177,10 +182,14 @@ def peer_gather_setup(out, world, rank, dev, dist, multicast=False):
     handed rank 0's slice r as their Y pointer, so the apply epilogue's stores travel over
     NVLink straight into the root's buffer: no separate gather pass and no HBM re-read of Y.
     A device-side barrier after each step orders the stores before anyone reads them.
-    Returns (the local buffer as [world][*out.shape] complex64, this rank's destination view,
-    the rendezvous handle).
+    Returns (the local buffer as [world][*out.shape] complex64, this rank's destination (view or address),
+    the rendezvous handle, the peer byte offsets for peer-all).
 
-    multicast: the destination is instead the buffer's NVLS multicast address + slice r
+    peer-all: the destination is this rank's own slice r, and the plan repeats every Y
+    store at the byte offsets to slice r of every peer's buffer (stap_params.out_peer_offset):
+    an all-gather by unicast stores, each GPU's NVLink ingress carrying only the peers' slices.
+
+    multimem: the destination is instead the buffer's NVLS multicast address + slice r
     (an int); the plan's out_multicast makes every Y store a multimem.st, so each rank's
     apply epilogue writes its slice into ALL ranks' buffers: an all-gather with no
     separate pass."""
@@ -189,13 +198,19 @@ def peer_gather_setup(out, world, rank, dev, dist, multicast=False):
     n = out.numel() * 2  # floats per rank slice
     buf = symm_mem.empty(world * n, dtype=torch.float32, device=dev)
     hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
-    if multicast:
+    offs = ()
+    if mode == "peer-all":
+        dst = buf[rank * n:(rank + 1) * n].view(torch.complex64).view(out.shape)
+        base = dst.data_ptr()
+        offs = tuple(hdl.get_buffer(j, (n,), torch.float32, rank * n).data_ptr() - base
+                     for j in range(world) if j != rank)
+    elif mode == "multimem":
         if not getattr(hdl, "multicast_ptr", 0):
             raise RuntimeError("--gather multimem: no NVLS multicast support on this box")
         dst = int(hdl.multicast_ptr) + rank * n * 4
     else:
         dst = hdl.get_buffer(0, (n,), torch.float32, rank * n).view(torch.complex64).view(out.shape)
-    return buf.view(torch.complex64).view((world,) + tuple(out.shape)), dst, hdl
+    return buf.view(torch.complex64).view((world,) + tuple(out.shape)), dst, hdl, offs
 
 
 def make_inputs(cfg, n_gpus, rank, cubes, steering_kind="ula"):
@@ -282,10 +297,11 @@ def main():
     ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
     ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto",
                     help="stap_run path (stap_params.path); auto = the library's measured choice")
-    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer", "multimem"],
+    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer", "peer-all", "multimem"],
                     help="gather the outputs after each step: nccl = NCCL all-gather (the default of a bare "
                          "--gather), nccl-root = NCCL gather to rank 0, peer = the kernels store Y straight "
-                         "into rank 0's symmetric buffer over NVLink, then a device barrier; multimem = an all-gather "
+                         "into rank 0's symmetric buffer over NVLink, then a device barrier; peer-all = an all-gather "
+                         "by the same stores into the own buffer and every peer's (out_n_peers); multimem = an all-gather "
                          "by multimem.st from the apply epilogue into every rank's symmetric buffer (NVLS) "
                          "(SURVEY 8(f) NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -334,15 +350,19 @@ def main():
     M = args.cubes
     dims = stap.Dims(cfg.C, cfg.T, gcfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
     mc = args.gather == "multimem" and world > 1
+    pall = args.gather == "peer-all" and world > 1
+    out = torch.empty(plan_shape_out(stap, dims, lo, cnt, b0, nb, M), dtype=torch.complex64, device=dev)
+    gather_buf, y_dst, peer, offs = None, out, None, ()
+    if args.gather in ("peer", "peer-all", "multimem") and world > 1:
+        gather_buf, y_dst, peer, offs = peer_gather_setup(out, world, rank, dev, dist, mode=args.gather)
     plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                         device=local_rank, path=args.path, out_multicast=mc)
+                         device=local_rank, path=args.path, out_multicast=mc, out_peer_offsets=offs)
     # an ordinary-store plan of the same shape for the e2e, stage and gather-check legs
     plan_u = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                           device=local_rank, path=args.path) if mc else plan
+                           device=local_rank, path=args.path) if (mc or pall) else plan
     stream = torch.cuda.current_stream(dev)
     cube = torch.from_numpy(x_h).to(dev)
     steer = torch.from_numpy(st_h).to(dev)
-    out = torch.empty(plan.out_shape, dtype=torch.complex64, device=dev)
     info = torch.empty(plan.info_shape, dtype=torch.int32, device=dev)
     staged = plan.description.startswith("staged")
     if staged:
@@ -350,13 +370,8 @@ def main():
         wts = torch.empty(plan.weights_shape, dtype=torch.complex64, device=dev)
         gam = torch.empty(plan.info_shape + (cfg.S,), dtype=torch.float32, device=dev)
     ws = plan.workspace()
-    gather_buf = None
-    y_dst = out  # where the kernels store Y
-    peer = None
-    if args.gather and world > 1:
-        if args.gather in ("peer", "multimem"):
-            gather_buf, y_dst, peer = peer_gather_setup(out, world, rank, dev, dist, multicast=mc)
-        elif args.gather == "nccl-root":
+    if args.gather and world > 1 and peer is None:
+        if args.gather == "nccl-root":
             # NCCL has no complex type: gather float32 views
             gather_buf = [torch.empty(out.numel() * 2, dtype=torch.float32, device=dev)
                           for _ in range(world)] if rank == 0 else None
@@ -472,7 +487,7 @@ def main():
             stap.stap_run(plan_u.handle, cube, steer, out, info, ws, plan_u.workspace_bytes, s_)
         ref = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
         dist.all_gather_into_tensor(ref.view(-1), out.view(-1))
-        ok = torch.tensor([1.0 if (rank != 0 and not mc) or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
+        ok = torch.tensor([1.0 if (rank != 0 and not (mc or pall)) or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
                            else 0.0], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         gather_check = "bitwise equal to ncclAllGather" if ok.item() == 1.0 else "MISMATCH vs ncclAllGather"

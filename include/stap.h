@@ -98,6 +98,17 @@ typedef struct {
                                 stream's work).  stap_run_host rejects 1 (host `out`)
                                 with STAP_ERR_UNSUPPORTED; any other value is
                                 STAP_ERR_BAD_DIMS.                                         */
+    int32_t out_n_peers;     /* ABI v3.  0..7 (else STAP_ERR_BAD_DIMS; > 0 together with
+                                out_multicast is STAP_ERR_BAD_DIMS).  Every Y store to `out`
+                                is repeated at out + out_peer_offset[i] (bytes), i < out_n_peers:
+                                peer-mapped copies of the same output slice in the other
+                                ranks' buffers (e.g. torch symmetric memory's get_buffer), so
+                                the apply epilogue performs an all-gather by unicast stores
+                                over NVLink.  Offsets must be multiples of 16
+                                (else STAP_ERR_MISALIGNED); the caller guarantees each
+                                out + offset range is mapped and writable.  stap_run_host
+                                rejects out_n_peers > 0 with STAP_ERR_UNSUPPORTED.           */
+    int64_t out_peer_offset[7];
 } stap_params;
 
 /* stap_run path.  AUTO picks the measured-faster one: the staged path when both its

@@ -52,6 +52,7 @@ class stap_params(ctypes.Structure):
         ("diag_load", ctypes.c_float), ("dop_begin", ctypes.c_int32), ("dop_count", ctypes.c_int32),
         ("cube_bin0", ctypes.c_int32), ("cube_bins", ctypes.c_int32), ("batch", ctypes.c_int32),
         ("device", ctypes.c_int32), ("path", ctypes.c_int32), ("out_multicast", ctypes.c_int32),
+        ("out_n_peers", ctypes.c_int32), ("out_peer_offset", ctypes.c_int64 * 7),
     ]
 
 
@@ -178,7 +179,7 @@ class StapPlan:
 
     def __init__(self, dims: Dims, dop_begin: int = 0, dop_count: int | None = None, cube_bin0: int = 0,
                  cube_bins: int | None = None, batch: int = 1, device: int = 0, path: str = "auto",
-                 out_multicast: bool = False):
+                 out_multicast: bool = False, out_peer_offsets=()):
         self.dims = dims
         self.dop_begin = dop_begin
         self.dop_count = dims.D if dop_count is None else dop_count
@@ -188,7 +189,8 @@ class StapPlan:
         self.device = device
         self.params = stap_params(dims.C, dims.T, dims.D, dims.R, dims.K, dims.S, float(dims.lam), dop_begin,
                                   self.dop_count, cube_bin0, self.cube_bins, batch, device,
-                                  PATHS[path], int(bool(out_multicast)))
+                                  PATHS[path], int(bool(out_multicast)), len(out_peer_offsets),
+                                  (ctypes.c_int64 * 7)(*out_peer_offsets))
         self.handle = stap_plan_create(self.params)
         self.workspace_bytes = stap_plan_workspace_bytes(self.handle, False)
         self.host_workspace_bytes = stap_plan_workspace_bytes(self.handle, True)

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __r
     for (int k = 0; k < SMAX; ++k)
       if (k < S)
         st_y(reinterpret_cast<float4*>(yb + (long long)k * p.R + j),
-             make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y), p.y_mc);
+             make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y), p);
   }
 }
 

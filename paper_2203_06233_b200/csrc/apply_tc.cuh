@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
       for (int k = 0; k < 8; ++k) {
         const float re = a[k] + c[k];                                  // Out[m][k]
         const float o = __shfl_xor_sync(0xffffffffu, b[k] + d[k], 1);  // partner row's Out[.][S+k]
-        st_y(yp, fmaf(sg, o, re), p.y_mc);
+        st_y(yp, fmaf(sg, o, re), p);
         yp += 2 * R;
       }
     };

@@ -14,24 +14,35 @@ struct KParams {
   int dop_begin, dop_count, bin0, nbins, batch;
   long long cube_stride;  // complex elements per cube in the batch = nbins*C*R
   int y_mc;               // stap_params.out_multicast: Y is an NVLS multicast address
+  int y_np;               // stap_params.out_n_peers: extra copies of every Y store ...
+  long long y_off[7];     // ... at these byte offsets from the store address (peer-mapped buffers)
 };
 
 // Y stores.  With p.y_mc the output pointer is a multicast (NVLS) address: one
-// multimem.st writes the value into every rank's copy of the buffer over NVSwitch
-// (the all-gather happens in the store; include/stap.h out_multicast).
-__device__ __forceinline__ void st_y(float* a, float v, int mc) {
-  if (mc) asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
-  else *a = v;
+// multimem.st writes the value into every rank's copy of the buffer over NVSwitch.
+// Otherwise the value is stored at the address and, for each of the p.y_np peer
+// offsets, at address + offset (a peer-mapped copy of the same slice): an
+// all-gather by unicast stores from the epilogue (include/stap.h out_n_peers).
+__device__ __forceinline__ void mm_st(float* a, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
 }
-__device__ __forceinline__ void st_y(float2* a, float2 v, int mc) {
-  if (mc) asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(a), "f"(v.x), "f"(v.y) : "memory");
-  else *a = v;
+__device__ __forceinline__ void mm_st(float2* a, float2 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(a), "f"(v.x), "f"(v.y) : "memory");
 }
-__device__ __forceinline__ void st_y(float4* a, float4 v, int mc) {
-  if (mc)
-    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x), "f"(v.y),
-                 "f"(v.z), "f"(v.w) : "memory");
-  else *a = v;
+__device__ __forceinline__ void mm_st(float4* a, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w) : "memory");
+}
+template <class V>
+__device__ __forceinline__ void st_y(V* a, V v, const KParams& p) {
+  if (p.y_mc) {
+    mm_st(a, v);
+    return;
+  }
+  *a = v;
+#pragma unroll
+  for (int i = 0; i < 7; ++i)
+    if (i < p.y_np) *reinterpret_cast<V*>(reinterpret_cast<char*>(a) + p.y_off[i]) = v;
 }
 
 // Local row of the cube buffer holding global bin a (a may be outside [0, D)):

@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
 #pragma unroll
         for (int k = 0; k < SMAX; ++k)
           if (k < S) {
-            st_y(yb + (long long)k * p.R + j, acc0[k], p.y_mc);
-            if (two) st_y(yb + (long long)k * p.R + j2, acc1[k], p.y_mc);
+            st_y(yb + (long long)k * p.R + j, acc0[k], p);
+            if (two) st_y(yb + (long long)k * p.R + j2, acc1[k], p);
           }
       }
     }

@@ -303,6 +303,9 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   if (C <= 0 || T <= 0 || D <= 0 || R <= 0 || K <= 0 || S <= 0 || p->batch <= 0) return STAP_ERR_BAD_DIMS;
   if (p->path < STAP_PATH_AUTO || p->path > STAP_PATH_STAGED) return STAP_ERR_BAD_DIMS;
   if (p->out_multicast != 0 && p->out_multicast != 1) return STAP_ERR_BAD_DIMS;
+  if (p->out_n_peers < 0 || p->out_n_peers > 7 || (p->out_n_peers > 0 && p->out_multicast)) return STAP_ERR_BAD_DIMS;
+  for (int i = 0; i < p->out_n_peers; ++i)
+    if (p->out_peer_offset[i] % 16 != 0) return STAP_ERR_MISALIGNED;
   if (R % K != 0 || T > D) return STAP_ERR_BAD_DIMS;
   if (!(p->diag_load >= 0.0f) || !std::isfinite(p->diag_load)) return STAP_ERR_BAD_DIMS;
   if (p->dop_begin < 0 || p->dop_count <= 0 || (long long)p->dop_begin + p->dop_count > D)
@@ -336,6 +339,8 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   kp.bin0 = p->cube_bin0; kp.nbins = p->cube_bins; kp.batch = p->batch;
   kp.cube_stride = (long long)p->cube_bins * C * R;
   kp.y_mc = p->out_multicast;
+  kp.y_np = p->out_n_peers;
+  for (int i = 0; i < 7; ++i) kp.y_off[i] = i < p->out_n_peers ? (long long)p->out_peer_offset[i] : 0;
   pl->units = (long long)p->batch * p->dop_count * kp.B;
 
   // K1: bins per CTA -- the largest run whose lag blocks fit 256 threads with
@@ -632,7 +637,7 @@ stap_status stap_run(const stap_plan* pl, const stap_c64* cube, const stap_c64* 
 stap_status stap_run_host(const stap_plan* pl, const stap_c64* h_cube, const stap_c64* h_steering, stap_c64* h_out,
                           int32_t* h_info, void* workspace, size_t workspace_bytes, cudaStream_t st) {
   if (!pl || !h_cube || !h_steering || !h_out || !h_info || !workspace) return STAP_ERR_NULL_ARG;
-  if (pl->prm.out_multicast) return STAP_ERR_UNSUPPORTED;  // a host `out` is not a multicast address
+  if (pl->prm.out_multicast || pl->prm.out_n_peers) return STAP_ERR_UNSUPPORTED;  // a host `out` is not a multicast address
   size_t need = 0;
   stap_plan_workspace_bytes(pl, 1, &need);
   if (workspace_bytes < need) return STAP_ERR_BAD_DIMS;

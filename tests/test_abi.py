@@ -66,6 +66,8 @@ def _params(pkg, **kw):
     (dict(cube_bins=10, dop_count=20), 2),                      # window does not cover the owned bins
     (dict(path=3), 2), (dict(path=-1), 2),                      # not a stap_path
     (dict(out_multicast=2), 2), (dict(out_multicast=-1), 2),    # not 0 or 1 (ABI v3)
+    (dict(out_n_peers=8), 2), (dict(out_n_peers=-1), 2), (dict(out_n_peers=1, out_multicast=1), 2),
+    (dict(out_n_peers=1, out_peer_offset=(ctypes.c_int64 * 7)(8)), 4),  # offset not a multiple of 16
     (dict(n_chan=9, tdof=7), 3), (dict(n_steering=33), 3),
     (dict(training_block=7, n_range=511), 3), (dict(n_chan=8, tdof=9), 3),
 ])

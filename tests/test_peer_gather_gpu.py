@@ -19,13 +19,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gather", ["peer", "multimem"])
+@pytest.mark.parametrize("gather", ["peer", "peer-all", "multimem"])
 @pytest.mark.parametrize("config", ["tiny", "small", "medium"])
 def test_peer_gather_bitwise_vs_nccl(config, gather):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str({"tiny": 29611, "small": 29612, "medium": 29613}[config] + (10 if gather == "multimem" else 0)),
+           "--master-addr", "127.0.0.1", "--master-port", str({"tiny": 29611, "small": 29612, "medium": 29613}[config] + {"peer": 0, "peer-all": 5, "multimem": 10}[gather]),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--steps", "2", "--warmup", "3",
            "--gather", gather, "--no-stages", "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
