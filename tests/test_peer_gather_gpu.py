@@ -1,7 +1,8 @@
 """Fused apply -> gather over NVLink peer stores (8(e) collective row).
 
 Two ranks, one GPU each: every rank's kernels store Y straight into rank 0's symmetric
-buffer (bench.py --gather peer), or, with multimem, every Y store is a multimem.st to the
+buffer (bench.py --gather peer); with peer-all every Y store is written locally and
+repeated into the peer's buffer (stap_params.out_n_peers); with multimem, every Y store is a multimem.st to the
 buffer's NVLS multicast address and lands in both ranks' buffers (--gather multimem).
 bench.py compares the gathered buffer (rank 0; every rank for multimem) with an NCCL
 all-gather of the same outputs and reports "gather_check"; the test requires bitwise equality.
