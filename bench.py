@@ -521,7 +521,7 @@ def main():
         dist.destroy_process_group()
 
 
-def stage_fractions(stap, plan_u, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
+def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
     import torch
     s_ = stap._stream(stream, dev_idx)
     cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=cube.device)
@@ -572,7 +572,7 @@ def stage_fractions(stap, plan_u, cube, steer, cfg, M, pk, stream, dev_idx, reps
     return res
 
 
-def e2e_measure(stap, plan_u, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
+def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
     import torch
     hc = torch.from_numpy(x_h).pin_memory()
     hs = torch.from_numpy(st_h).pin_memory()

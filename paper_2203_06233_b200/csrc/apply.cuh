@@ -94,9 +94,12 @@ __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __r
     }
 #pragma unroll
     for (int k = 0; k < SMAX; ++k)
-      if (k < S)
-        st_y(reinterpret_cast<float4*>(yb + (long long)k * p.R + j),
-             make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y), p);
+      if (k < S) {
+        float4* ya = reinterpret_cast<float4*>(yb + (long long)k * p.R + j);
+        const float4 yv = make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y);
+        if (p.y_mc | p.y_np) st_y(ya, yv, p);
+        else *ya = yv;
+      }
   }
 }
 

@@ -218,12 +218,20 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
       float* yp = reinterpret_cast<float*>(out + (long long)x.nd * S * R + (long long)(8 * hq) * R +
                                            (long long)x.b * K + x.mt * 64 + jj) + part;
       const float sg = part ? -1.f : 1.f;  // Re: own + partner; Im: own - partner
+      float yv[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float re = a[k] + c[k];                                  // Out[m][k]
         const float o = __shfl_xor_sync(0xffffffffu, b[k] + d[k], 1);  // partner row's Out[.][S+k]
-        st_y(yp, fmaf(sg, o, re), p);
-        yp += 2 * R;
+        yv[k] = fmaf(sg, o, re);
+      }
+      // the remote-store branch is taken once per tile, outside the store loop
+      if (p.y_mc | p.y_np) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st_y(yp + (long long)k * 2 * R, yv[k], p);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) yp[(long long)k * 2 * R] = yv[k];
       }
     };
 

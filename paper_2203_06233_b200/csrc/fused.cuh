@@ -243,12 +243,21 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
             }
           }
         }
+        if (p.y_mc | p.y_np) {  // remote stores: branch once per pass, outside the store loop
 #pragma unroll
-        for (int k = 0; k < SMAX; ++k)
-          if (k < S) {
-            st_y(yb + (long long)k * p.R + j, acc0[k], p);
-            if (two) st_y(yb + (long long)k * p.R + j2, acc1[k], p);
-          }
+          for (int k = 0; k < SMAX; ++k)
+            if (k < S) {
+              st_y(yb + (long long)k * p.R + j, acc0[k], p);
+              if (two) st_y(yb + (long long)k * p.R + j2, acc1[k], p);
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < SMAX; ++k)
+            if (k < S) {
+              yb[(long long)k * p.R + j] = acc0[k];
+              if (two) yb[(long long)k * p.R + j2] = acc1[k];
+            }
+        }
       }
     }
     group_sync<G>(bar_id);
