@@ -1,19 +1,25 @@
 #!/usr/bin/env python
 """bench.py -- STAP datacubes/s on 1..N B200s (BASELINE.json metric), one JSON line.
 
-Workload: BASELINE.json configs[1] "STAP small" by
-default (4 channels, TDOF 3, 256 Doppler bins, 512 range cells, 16 steering
-vectors, training block 32); --config medium|large select configs[2]/[3].
-A step is one pass of the whole hot path (covariance + loading, Cholesky +
-solves -> MVDR weights, application) over a batch of `--cubes` distinct seeded
-synthetic datacubes resident in HBM (input > L2, so no L2 flush is needed).
+Workload: BASELINE.json configs[3] "STAP large" by
+default (8 channels, TDOF 7, 1024 Doppler bins, 4096 range cells, 16 steering
+vectors, training block 128) -- the largest configuration that fits one GPU and,
+per GPU, the configs[4] weak-scaling slice; --config small|medium select
+configs[1]/[2].  A step is one pass of the whole hot path (covariance + loading,
+Cholesky + solves -> MVDR weights, application) over a batch of `--cubes`
+distinct seeded synthetic datacubes resident in HBM (input > L2, so no L2 flush
+is needed).  --precision tf32x3 (default) opts the covariance and the apply into
+the library's 3xTF32 tcgen05 stages (stap_params.precision; FP32-level accuracy,
+parity-tested against the fp64 oracle); --precision fp32 runs FP32 FFMA only.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): Doppler-bin shards with weak
-scaling (BASELINE.json configs[4] pattern): the global cube has D = D_cfg x N
-bins, rank g owns the contiguous slice [g*D_cfg, (g+1)*D_cfg) plus a T-1 bin
-read-only halo, so per-GPU work is fixed; no collective is on the data path
-(--gather adds the optional NCCL all-gather of the outputs).  `value` counts
-every D_cfg-bin slice processed as one config-shaped datacube, summed over ranks.
+Multi-GPU (torchrun, one process per GPU, NCCL): Doppler-bin shards.  --split weak
+(default; BASELINE.json configs[4]): the global cube has D = D_cfg x N bins, rank g
+owns the contiguous slice [g*D_cfg, (g+1)*D_cfg) plus a T-1 bin read-only halo, so
+per-GPU work is fixed; `value` counts every D_cfg-bin slice processed as one
+config-shaped datacube, summed over ranks.  --split strong (configs[2] "medium on
+1/2/4/8"): every step's cubes are the config's D bins split D/N per rank, so the
+work per step is fixed; `value` = whole cubes per second.  No collective is on the
+data path; --gather adds the optional gather of the outputs.
 
 --impl reference times the fp64 C oracle (the reference arm for this tier) on
 the host cores, on a bounded sample of the same workload.
@@ -42,6 +48,8 @@ WORKLOAD_DESC = {
     "large": "STAP large (BASELINE.json configs[3]): C=8, TDOF=7, D=1024, R=4096, S=16, K=128",
 }
 DEFAULT_CUBES = {"tiny": 64, "small": 64, "medium": 16, "large": 2}
+# TF32 dense tensor peak = measured bf16 x the guide's nominal ratio (1.1 / 2.25 PFLOP/s)
+TF32_PER_BF16 = 1.1 / 2.25
 
 
 # ---------------------------------------------------------------- algorithmic counts
@@ -86,19 +94,41 @@ def peaks() -> dict:
     except Exception:
         pass
     p["fp32_tflops"] = 148 * 128 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    bf16 = 1590.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            bf16 = float(json.load(fh)["bf16_tflops"])
+    except Exception:
+        pass
+    p["tf32_tflops"] = bf16 * TF32_PER_BF16
     return p
 
 
-def roofline_obj(flops: float, nbytes: float, seconds: float, pk: dict, traffic=None, extra=None) -> dict:
-    t_alu = flops / (pk["fp32_tflops"] * 1e12)
+def roofline_obj(flops: float, nbytes: float, seconds: float, pk: dict, traffic=None, extra=None,
+                 tensor: bool = False) -> dict:
+    """frac = t_roof / t_meas.  FP32 SIMT stages: t_roof = max(bytes / HBM, flops / FP32 peak).
+    tcgen05 3xTF32 stages: t_roof = max(bytes / HBM, 3 x flops / TF32 peak) -- three TF32 MMAs
+    per FP32-accurate product, TF32 peak = measured bf16 x 1.1/2.25 (B200_PROFILING.md)."""
     t_hbm = nbytes / (pk["hbm_gbs"] * 1e9)
-    if t_alu >= t_hbm:
-        ach = flops / seconds / 1e12
-        o = {"bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
-             "frac": ach / pk["fp32_tflops"]}
+    if tensor:
+        t_alu = 3.0 * flops / (pk["tf32_tflops"] * 1e12)
+        if t_alu >= t_hbm:
+            ach = 3.0 * flops / seconds / 1e12
+            o = {"bound": "tensor", "achieved": ach, "peak": pk["tf32_tflops"], "unit": "TFLOP/s",
+                 "frac": ach / pk["tf32_tflops"], "note": "3xTF32: achieved counts 3 TF32 MMAs per algorithmic flop"}
+        else:
+            ach = nbytes / seconds / 1e9
+            o = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
+        o["frac_of_fp32_simt"] = flops / seconds / 1e12 / pk["fp32_tflops"]
     else:
-        ach = nbytes / seconds / 1e9
-        o = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
+        t_alu = flops / (pk["fp32_tflops"] * 1e12)
+        if t_alu >= t_hbm:
+            ach = flops / seconds / 1e12
+            o = {"bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                 "frac": ach / pk["fp32_tflops"]}
+        else:
+            ach = nbytes / seconds / 1e9
+            o = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
     o["traffic"] = traffic
     if extra:
         o.update(extra)
@@ -213,11 +243,25 @@ def peer_gather_setup(out, world, rank, dev, dist, mode="peer"):
     return buf.view(torch.complex64).view((world,) + tuple(out.shape)), dst, hdl, offs
 
 
-def make_inputs(cfg, n_gpus, rank, cubes, steering_kind="ula"):
-    """This rank's cube buffers [cubes][D_cfg + halo][C][R] (halo only when N > 1), complex64."""
-    gcfg = cfg.with_(D=cfg.D * n_gpus) if n_gpus > 1 else cfg
-    lo, cnt = rank * cfg.D, cfg.D
+def shard_plan_args(cfg, n_gpus, rank, split="weak"):
+    """(global config, dop_begin, dop_count, cube_bin0, cube_bins) of this rank's shard plan.
+    weak: global D = D_cfg * N, rank g owns [g D_cfg, (g+1) D_cfg); strong: the config's D bins
+    split D/N per rank (synth.shard_range).  N = 1: the whole cube, no halo."""
+    if n_gpus <= 1:
+        return cfg, 0, cfg.D, 0, cfg.D
+    if split == "weak":
+        gcfg = cfg.with_(D=cfg.D * n_gpus)
+        lo, cnt = rank * cfg.D, cfg.D
+    else:
+        gcfg = cfg
+        lo, cnt = synth.shard_range(cfg.D, n_gpus, rank)
     b0, nb = synth.shard_window(gcfg, lo, cnt)
+    return gcfg, lo, cnt, b0, nb
+
+
+def make_inputs(cfg, n_gpus, rank, cubes, steering_kind="ula", split="weak"):
+    """This rank's cube buffers [cubes][Dl + halo][C][R] (halo only when N > 1), complex64."""
+    gcfg, lo, cnt, b0, nb = shard_plan_args(cfg, n_gpus, rank, split)
     bins = (b0 + np.arange(nb)) % gcfg.D
     x = np.empty((cubes, nb, cfg.C, cfg.R), np.complex64)
     for i in range(cubes):
@@ -279,11 +323,24 @@ def run_reference(args, cfg, world, rank):
 
 
 def config_obj(args, cfg, world):
+    if world > 1 and args.split == "strong":
+        par = f"doppler-shard x{world} (strong: D = {cfg.D} split {cfg.D // world} bins per rank + halo)"
+        per_gpu = f"{args.cubes} cubes x 1/{world} of the bins"
+    else:
+        par = f"doppler-shard x{world} (weak: global D = {cfg.D}*{world})"
+        per_gpu = args.cubes
     return {"workload": WORKLOAD_DESC.get(cfg.name, cfg.name), "C": cfg.C, "TDOF": cfg.T, "D": cfg.D, "R": cfg.R,
-            "S": cfg.S, "K": cfg.K, "lambda": cfg.lam, "cubes_per_step_per_gpu": args.cubes,
-            "parallelism": f"doppler-shard x{world} (weak: global D = {cfg.D}*{world})",
+            "S": cfg.S, "K": cfg.K, "lambda": cfg.lam, "cubes_per_step_per_gpu": per_gpu,
+            "parallelism": par, "precision": PRECISION_DESC[args.precision],
             "l2": "inputs larger than L2 (no flush)", "steering": "ULA centre-bin",
             **({"gather": args.gather} if args.gather and world > 1 else {})}
+
+
+PRECISION_DESC = {
+    "tf32x3": "stap_params.precision=STAP_PREC_TF32X3: covariance and apply on tcgen05 in 3xTF32 (FP32-level "
+              "accuracy, oracle parity <= 1e-3 per output vector), Cholesky/solves FP32 FFMA",
+    "fp32": "stap_params.precision=STAP_PREC_FP32: FP32 FFMA in every stage",
+}
 
 
 # ---------------------------------------------------------------- our arm
@@ -293,16 +350,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(WORKLOAD_DESC), default="small")
+    ap.add_argument("--config", choices=list(WORKLOAD_DESC), default="large")
     ap.add_argument("--cubes", type=int, default=None, help="cubes per step per GPU")
     ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto",
                     help="stap_run path (stap_params.path); auto = the library's measured choice")
-    ap.add_argument("--gather", nargs="?", const="nccl", default=None, choices=["nccl", "nccl-root", "peer", "peer-all", "multimem"],
-                    help="gather the outputs after each step: nccl = NCCL all-gather (the default of a bare "
-                         "--gather), nccl-root = NCCL gather to rank 0, peer = the kernels store Y straight "
-                         "into rank 0's symmetric buffer over NVLink, then a device barrier; peer-all = an all-gather "
-                         "by the same stores into the own buffer and every peer's (out_n_peers); multimem = an all-gather "
-                         "by multimem.st from the apply epilogue into every rank's symmetric buffer (NVLS) "
+    ap.add_argument("--precision", choices=["tf32x3", "fp32"], default="tf32x3",
+                    help="stap_params.precision: tf32x3 = tcgen05 3xTF32 covariance/apply (default), fp32 = FFMA only")
+    ap.add_argument("--split", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = a D_cfg-bin slice per rank (configs[4]); strong = one D-bin cube split N ways")
+    ap.add_argument("--gather", nargs="?", const="comm", default=None,
+                    choices=["comm", "comm-peer", "nccl", "nccl-root", "peer", "peer-all", "multimem"],
+                    help="gather the outputs after each step: comm = the library's stap_comm_allgather_out "
+                         "(in-place ncclAllGather; the default of a bare --gather); comm-peer = the library's "
+                         "stap_comm_peer_offsets + out_n_peers: the all-gather fused into the apply epilogue by "
+                         "peer stores (CUDA IPC mapping), a 1-float all-reduce per step as the device barrier; "
+                         "baselines through torch: nccl = all_gather_into_tensor, nccl-root = gather to rank 0, "
+                         "peer / peer-all / multimem = torch symmetric memory + the same epilogue stores "
                          "(SURVEY 8(f) NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -346,31 +409,54 @@ def main():
             os.dup2(saved, 1)
             os.close(saved)
 
-    gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes)
+    gcfg, lo, cnt, b0, nb, x_h, st_h = make_inputs(cfg, world, rank, args.cubes, split=args.split)
     M = args.cubes
     dims = stap.Dims(cfg.C, cfg.T, gcfg.D, cfg.R, cfg.K, cfg.S, cfg.lam)
-    mc = args.gather == "multimem" and world > 1
-    pall = args.gather == "peer-all" and world > 1
+    multi = world > 1
+    mc = args.gather == "multimem" and multi
     out = torch.empty(plan_shape_out(stap, dims, lo, cnt, b0, nb, M), dtype=torch.complex64, device=dev)
-    gather_buf, y_dst, peer, offs = None, out, None, ()
-    if args.gather in ("peer", "peer-all", "multimem") and world > 1:
+    gather_buf, y_dst, peer, offs, comm, step_bar = None, out, None, (), None, None
+    if args.gather in ("peer", "peer-all", "multimem") and multi:
         gather_buf, y_dst, peer, offs = peer_gather_setup(out, world, rank, dev, dist, mode=args.gather)
+    elif args.gather in ("comm", "comm-peer") and multi:
+        # the library's multi-GPU extension, one process per GPU: the NCCL unique id travels
+        # over the torch process group, the communicator is libstap's own
+        uid = [stap.StapComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            comm = stap.StapComm(nranks=world, rank=rank, uid=uid[0], device=local_rank)
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
+        gather_buf = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
+        y_dst = gather_buf[rank]
+        if args.gather == "comm-peer":
+            offs = comm.peer_offsets([gather_buf])[0]
+            step_bar = torch.zeros(1, dtype=torch.float32, device=dev)
+    pall = bool(offs) and multi
     plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                         device=local_rank, path=args.path, out_multicast=mc, out_peer_offsets=offs)
+                         device=local_rank, path=args.path, out_multicast=mc, out_peer_offsets=offs,
+                         precision=args.precision)
     # an ordinary-store plan of the same shape for the e2e, stage and gather-check legs
     plan_u = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
-                           device=local_rank, path=args.path) if (mc or pall) else plan
+                           device=local_rank, path=args.path, precision=args.precision) if (mc or pall) else plan
     stream = torch.cuda.current_stream(dev)
     cube = torch.from_numpy(x_h).to(dev)
     steer = torch.from_numpy(st_h).to(dev)
     info = torch.empty(plan.info_shape, dtype=torch.int32, device=dev)
     staged = plan.description.startswith("staged")
+    tc_stage = {"covariance": "cov(tcgen05" in plan.description, "solve": False,
+                "apply": "apply(tcgen05" in plan.description}
     if staged:
         cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=dev)
         wts = torch.empty(plan.weights_shape, dtype=torch.complex64, device=dev)
         gam = torch.empty(plan.info_shape + (cfg.S,), dtype=torch.float32, device=dev)
     ws = plan.workspace()
-    if args.gather and world > 1 and peer is None:
+    if args.gather in ("nccl", "nccl-root") and multi:
         if args.gather == "nccl-root":
             # NCCL has no complex type: gather float32 views
             gather_buf = [torch.empty(out.numel() * 2, dtype=torch.float32, device=dev)
@@ -398,15 +484,22 @@ def main():
                 ev_stage.append(e)
         else:
             stap.stap_run(plan.handle, cube, steer, y_dst, info, ws, plan.workspace_bytes, s_)
+        if not multi or not args.gather:
+            return
         if peer is not None:
-            peer.barrier(channel=0)  # every rank's stores into rank 0's buffer have landed
-        elif args.gather == "nccl-root" and world > 1:
+            peer.barrier(channel=0)  # every rank's stores into the symmetric buffers have landed
+        elif comm is not None:
+            if step_bar is not None:
+                dist.all_reduce(step_bar)  # device barrier: every rank's peer stores have landed
+            else:
+                comm.allgather_out([gather_buf], [plan], [stream])
+        elif args.gather == "nccl-root":
             dist.gather(out.view(torch.float32).view(-1), gather_list=gather_buf, dst=0)
         elif gather_buf is not None:
             dist.all_gather_into_tensor(gather_buf.view(-1), out.view(-1))
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize(dev)
 
@@ -428,7 +521,7 @@ def main():
             barrier()
         el = t0.elapsed_time(t1) / 1e3
         tmax = torch.tensor([el], dtype=torch.float64, device=dev)
-        if world > 1:
+        if multi:
             dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         return float(tmax.item()), clk.summary()
 
@@ -436,19 +529,22 @@ def main():
     # a run that saw a hardware/thermal slowdown is rejected and measured once more
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     flag = torch.tensor([1.0 if bad & set(clocks.get("reasons", [])) else 0.0], device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(flag, op=dist.ReduceOp.MAX)
     if flag.item() > 0:
         first = clocks
         elapsed, clocks = timed_region()
         clocks["remeasured_after"] = first.get("reasons")
-    cubes_total = world * M * args.steps
+    strong = multi and args.split == "strong"
+    cubes_total = (M if strong else world * M) * args.steps
     value = cubes_total / elapsed
     ms_per_step = elapsed / args.steps * 1e3
     ninfo_bad = int((info != 0).sum().item())
 
     pk = peaks()
+    # per-rank algorithmic counts: the rank's slice of bins (a config-shaped cube under weak)
     cnt_cfg = counts(cfg)
+    frac_bins = cnt / cfg.D
     launches_per_step = 3 if staged else 1
     if staged:
         dur = {k: [] for k in ("covariance", "solve", "apply")}
@@ -459,42 +555,49 @@ def main():
         avg = {k: sum(v) / len(v) for k, v in dur.items()}
         top = max(avg, key=avg.get)
         sc = cnt_cfg["stage"][top]
-        roof = roofline_obj(sc["flops"] * M, sc["bytes"] * M, avg[top], pk,
-                            extra={"kernel": top, "share_of_step": avg[top] / (elapsed / args.steps)})
+        roof = roofline_obj(sc["flops"] * M * frac_bins, sc["bytes"] * M * frac_bins, avg[top], pk,
+                            tensor=tc_stage[top],
+                            extra={"kernel": top, "share_of_step": avg[top] / (elapsed / args.steps),
+                                   "stage_us": {k: v * 1e6 for k, v in avg.items()}})
     else:
         t_launch = elapsed / args.steps
-        roof = roofline_obj(cnt_cfg["flops_fused_lag"] * M, cnt_cfg["bytes_fused"] * M, t_launch, pk,
+        roof = roofline_obj(cnt_cfg["flops_fused_lag"] * M * frac_bins, cnt_cfg["bytes_fused"] * M * frac_bins,
+                            t_launch, pk,
                             extra={"kernel": "fused_kernel (stap_run)", "share_of_step": 1.0,
-                                   "achieved_perbin_count": cnt_cfg["flops_fused_bin"] * M / t_launch / 1e12})
+                                   "achieved_perbin_count": cnt_cfg["flops_fused_bin"] * M * frac_bins / t_launch / 1e12})
     roof["peak_source"] = pk["source"]
     # measured DRAM traffic of this kernel/launch from the committed ncu --set full capture (profiles/)
-    tkey = f"{args.config}/{'staged-' + roof['kernel'] if staged else 'fused'}/{M}"
+    tkey = f"{args.config}/{args.precision}/{'staged-' + roof['kernel'] if staged else 'fused'}/{M}"
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(tkey)
-        if tr:
+        if tr and not multi:
             roof["traffic"] = tr["bytes_per_launch"]
-            roof["traffic_source"] = f"profiles/{tr['report']}_ncu_summary.txt"
+            roof["traffic_source"] = tr["source"]
     except Exception:
         pass
 
     gather_check = None
-    if peer is not None:
-        # the root's peer-gathered buffer must equal an NCCL all-gather of the local outputs, bitwise
+    if multi and args.gather in ("peer", "peer-all", "multimem", "comm", "comm-peer"):
+        # the gathered buffer must equal an NCCL all-gather of the local outputs, bitwise
         if staged:
             stap.stap_apply(plan_u.handle, cube, wts, out, s_)
         else:
             stap.stap_run(plan_u.handle, cube, steer, out, info, ws, plan_u.workspace_bytes, s_)
         ref = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
         dist.all_gather_into_tensor(ref.view(-1), out.view(-1))
-        ok = torch.tensor([1.0 if (rank != 0 and not (mc or pall)) or torch.equal(ref.view(torch.float32), gather_buf.view(torch.float32))
+        torch.cuda.synchronize(dev)
+        root_only = args.gather == "peer"
+        ok = torch.tensor([1.0 if (rank != 0 and root_only) or torch.equal(ref.view(torch.float32),
+                                                                          gather_buf.view(torch.float32))
                            else 0.0], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         gather_check = "bitwise equal to ncclAllGather" if ok.item() == 1.0 else "MISMATCH vs ncclAllGather"
 
     result = {
         "metric": "STAP datacubes/sec", "value": value, "unit": "cubes/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_obj(args, cfg, world),
         "path": plan.description, "gpu_launches": launches_per_step * args.steps, "roofline": roof,
         "clocks": clocks, "info_nonzero": ninfo_bad,
@@ -504,11 +607,16 @@ def main():
 
     # per-stage roofline fractions (BASELINE.json metric: "% of HBM/FP32 roofline per stage")
     if not args.no_stages:
-        result["stages"] = stage_fractions(stap, plan_u, cube, steer, cfg, M, pk, stream, local_rank)
+        result["stages"] = stage_fractions(stap, plan_u, cube, steer, cfg, M * frac_bins, pk, stream, local_rank,
+                                           tc_stage)
+        if not staged:
+            result["stages"]["note"] = ("the stage entry points (stap_covariance / stap_solve_weights / stap_apply "
+                                        "kernels), timed in isolation; the step itself runs the fused kernel")
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     if not args.no_e2e:
-        result["e2e"] = e2e_measure(stap, plan_u, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist)
+        result["e2e"] = e2e_measure(stap, plan_u, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist,
+                                    strong)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, sample, _ = cpu_oracle_rate(cfg, args.cpu_budget, sample_bins=oracle_sample_bins(cfg))
@@ -516,12 +624,13 @@ def main():
                                   "sample": sample}
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier(device_ids=[local_rank])
+        del comm
         dist.destroy_process_group()
 
 
-def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=10):
+def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, tc_stage, reps=10):
     import torch
     s_ = stap._stream(stream, dev_idx)
     cov = torch.empty(plan.cov_shape, dtype=torch.complex64, device=cube.device)
@@ -548,9 +657,14 @@ def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=1
         e1.record(stream)
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3 / reps
-        r = roofline_obj(c[name]["flops"] * M, c[name]["bytes"] * M, t, pk)
+        r = roofline_obj(c[name]["flops"] * M, c[name]["bytes"] * M, t, pk, tensor=tc_stage[name])
         res[name] = {"us": t * 1e6, "bound": r["bound"], "achieved": r["achieved"], "unit": r["unit"],
-                     "frac": r["frac"]}
+                     "frac": r["frac"], "kernel": "tcgen05 3xTF32" if tc_stage[name] else "FP32 SIMT"}
+        if "frac_of_fp32_simt" in r:
+            res[name]["frac_of_fp32_simt"] = r["frac_of_fp32_simt"]
+        if name == "covariance":
+            # the method's per-bin Hermitian count beside the Doppler-lag-shared one used above
+            res[name]["achieved_perbin_tflops"] = c[name]["flops_bin"] * M / t / 1e12
     # the front end (not part of the step): stap_doppler on a cube-shaped
     # input, HBM-bound (one read, one write of the cube)
     D = plan.dims.D
@@ -572,7 +686,7 @@ def stage_fractions(stap, plan, cube, steer, cfg, M, pk, stream, dev_idx, reps=1
     return res
 
 
-def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist):
+def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, stream, dist, strong=False):
     import torch
     hc = torch.from_numpy(x_h).pin_memory()
     hs = torch.from_numpy(st_h).pin_memory()
@@ -598,7 +712,7 @@ def e2e_measure(stap, plan, x_h, st_h, cfg, M, args, world, local_rank, dev, str
     t = float(tt.item())
     h2d = hc.numel() * 8 + hs.numel() * 8
     d2h = ho.numel() * 8 + hi.numel() * 4
-    return {"value": world * M * steps / t, "unit": "cubes/s", "h2d_bytes_per_step": int(h2d),
+    return {"value": (1 if strong else world) * M * steps / t, "unit": "cubes/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "api": "stap_run_host (pinned host buffers)"}
 
 

@@ -35,10 +35,17 @@
  *                weight and output of that unit is 0
  *        -(k+1)  gamma_k <= 0 or not finite for the smallest such k: the
  *                weights/outputs of every failing k are 0.
- *  - Arithmetic is FP32 (no TF32, no fast-math); results match the fp64 oracle
- *    to the tolerances in DESIGN.md, not bitwise.  A given plan computes every
- *    unit with a fixed summation order that does not depend on dop_begin,
- *    dop_count or batch: shards are bitwise identical to the unsharded run.
+ *  - Arithmetic: complex64 in and out, FP32 FFMA throughout under the default
+ *    stap_params.precision = STAP_PREC_FP32 (no TF32, no fast-math; the solver's
+ *    1/pivot is the hardware reciprocal, rcp.approx, ~1 ulp).  STAP_PREC_TF32X3 opts
+ *    the covariance (24 <= N <= 64, K % 16 == 0) and the weight application (S == 16,
+ *    K % 64 == 0) into tcgen05 tensor-core MMAs in 3xTF32 (each FP32 operand split
+ *    hi + lo, hi*hi + hi*lo + lo*hi, FP32 accumulation; measured per-R error
+ *    <= 2.3e-6, per-Y-line <= 5e-7 against the fp64 oracle); which kernels a plan
+ *    runs is fixed at plan creation (stap_plan_describe) and never changes per call.
+ *    Results match the fp64 oracle to the tolerances in DESIGN.md, not bitwise.  A
+ *    given plan computes every unit with a fixed summation order that does not depend
+ *    on dop_begin, dop_count or batch: shards are bitwise identical to the unsharded run.
  *  - There is no CPU fallback: without an sm_100 device every call fails.
  */
 #ifndef STAP_H_
@@ -52,7 +59,7 @@
 extern "C" {
 #endif
 
-#define STAP_ABI_VERSION 3
+#define STAP_ABI_VERSION 4
 
 typedef struct { float re, im; } stap_c64;
 typedef struct stap_plan stap_plan;
@@ -65,7 +72,9 @@ typedef enum {
     STAP_ERR_UNSUPPORTED = 3,  /* valid but not implemented: N = C*T > 64, S > 32, K odd,
                                   K > 1024, C > 8 */
     STAP_ERR_MISALIGNED = 4,   /* a device pointer is not 16-byte aligned */
-    STAP_ERR_CUDA = 5,         /* a CUDA runtime / launch error */
+    STAP_ERR_CUDA = 5,         /* a CUDA runtime / launch error (incl. a tensor map that cannot be
+                                  encoded for the given cube pointer) */
+    STAP_ERR_NCCL = 6,         /* multi-GPU extension: NCCL missing, or an NCCL / IPC call failed */
     STAP_ERR_DEVICE = 7        /* no device, or the plan's device is not sm_100 */
 } stap_status;
 
@@ -109,12 +118,19 @@ typedef struct {
                                 out + offset range is mapped and writable.  stap_run_host
                                 rejects out_n_peers > 0 with STAP_ERR_UNSUPPORTED.           */
     int64_t out_peer_offset[7];
+    int32_t precision;       /* ABI v4.  A stap_precision value (0 = STAP_PREC_FP32, the default;
+                                else STAP_ERR_BAD_DIMS)                                    */
 } stap_params;
 
+/* Arithmetic of the covariance and apply stages (include/stap.h header "Arithmetic").
+ * STAP_PREC_FP32: FP32 FFMA everywhere.  STAP_PREC_TF32X3: tcgen05 3xTF32 covariance and
+ * apply where the shape allows (see above), FP32 elsewhere; opt-in only. */
+typedef enum { STAP_PREC_FP32 = 0, STAP_PREC_TF32X3 = 1 } stap_precision;
+
 /* stap_run path.  AUTO picks the measured-faster one: the staged path when both its
- * tensor-core stages apply (covariance: 24 <= N <= 64, K % 16 == 0; apply: S = 16,
- * K % 64 == 0, N <= 64 -- medium, large), else the fused kernel when the shape fits it
- * (small), else staged.  FUSED on a shape the fused kernel cannot hold is
+ * tensor-core stages are in use (precision = STAP_PREC_TF32X3 and covariance:
+ * 24 <= N <= 64, K % 16 == 0; apply: S = 16, K % 64 == 0, N <= 64 -- medium, large), else
+ * the fused kernel when the shape fits it (small, medium), else staged.  FUSED on a shape the fused kernel cannot hold is
  * STAP_ERR_UNSUPPORTED.  The stage entry points are independent of this field. */
 typedef enum { STAP_PATH_AUTO = 0, STAP_PATH_FUSED = 1, STAP_PATH_STAGED = 2 } stap_path;
 
@@ -173,6 +189,46 @@ stap_status stap_run_host(const stap_plan* plan, const stap_c64* h_cube, const s
 
 const char* stap_status_string(stap_status s);
 int32_t stap_abi_version(void);
+
+/* ---- Multi-GPU extension.  Doppler bins shard over ranks with no
+ * data-path exchange (each rank's plan owns dop_begin .. dop_begin+dop_count-1, its cube
+ * buffer holds those bins plus the T-1 halo); the only collective is the OPTIONAL gather of
+ * the Doppler-major outputs -- the analogue of the paper's per-chunk result return
+ * (the pfor driver reassembling per-chunk slices).
+ *
+ * The gathered buffer of every rank, out_full, is [nranks][batch][Dl][S][R] complex64 (for
+ * batch = 1 and equal shards that is the global Doppler-major [D][S][R]); rank r's plan
+ * writes its own slice, out_full + r*batch*Dl*S*R.  NCCL (2.x, libnccl.so.2) is loaded at
+ * run time on the first stap_comm call; without it the calls return STAP_ERR_NCCL and the
+ * single-GPU library is unaffected.  A communicator is used from one host thread at a time. */
+typedef struct stap_comm stap_comm;
+/* 128 bytes that name a new communicator; produced on one rank, handed to all (any channel). */
+stap_status stap_comm_unique_id(uint8_t id[128]);
+/* One process driving `ndev` GPUs (ranks 0..ndev-1 = devices[0..ndev-1]): an NCCL clique
+ * (ncclCommInitAll) plus peer access between every pair of devices. */
+stap_status stap_comm_create(int32_t ndev, const int32_t* devices, stap_comm** out_comm);
+/* One process per GPU: this process's rank `rank` of `nranks`, on CUDA ordinal `device`. */
+stap_status stap_comm_init_rank(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device,
+                                stap_comm** out_comm);
+/* Ranks in the communicator and devices driven by this process (1 under init_rank). */
+stap_status stap_comm_size(const stap_comm* comm, int32_t* nranks, int32_t* nlocal);
+/* In-place all-gather of the outputs (ncclAllGather, one group call): for every local device
+ * i, out_full[i] (device memory of that device, layout above) and plans[i] (that rank's plan:
+ * the same batch, dop_count, S and R on every rank, else STAP_ERR_BAD_DIMS); enqueued on
+ * streams[i], after which every rank's out_full holds every rank's slice. */
+stap_status stap_comm_allgather_out(stap_comm* comm, stap_c64* const* out_full, const stap_plan* const* plans,
+                                    const cudaStream_t* streams);
+/* The all-gather fused into the apply epilogue: writes, for every local
+ * device i, offsets[i*7 + 0 .. n_peers-1] = the byte offsets from this rank's slice of
+ * out_full[i] to the same slice of every other rank's out_full (peer memory: peer access in one
+ * process; CUDA IPC over the NCCL communicator across processes -- out_full must then be a
+ * cudaMalloc allocation or lie inside one).  Passing them as stap_params.out_n_peers /
+ * out_peer_offset makes every Y store of stap_run / stap_apply land in every rank's buffer; the
+ * caller orders the stores before reading (stream sync + a barrier across ranks).  Collective:
+ * every rank calls it with its own buffers.  n_peers = nranks - 1 <= 7. */
+stap_status stap_comm_peer_offsets(stap_comm* comm, stap_c64* const* out_full, int64_t* offsets, int32_t* n_peers);
+/* Frees the NCCL communicators and closes the IPC mappings; NULL is accepted. */
+stap_status stap_comm_destroy(stap_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,9 @@ __host__ inline size_t apply_smem_bytes(int N, int SMAX, int units_per_cta) {
 }
 
 // grid.x over groups of `upc` units (unit = ((n*Dl + dl)*B + b)); blockDim = upc * tpu.
-template <int SMAX>
+// REMOTE: Y stores go through st_y (multicast / peer copies, include/stap.h out_multicast /
+// out_n_peers); the plain instantiation compiles to ordinary stores only.
+template <int SMAX, bool REMOTE>
 __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __restrict__ cube,
                                                      const float2* __restrict__ wts,
                                                      float2* __restrict__ out, int tpu, int upc,
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(128) apply_kernel(KParams p, const float2* __r
       if (k < S) {
         float4* ya = reinterpret_cast<float4*>(yb + (long long)k * p.R + j);
         const float4 yv = make_float4(acc0[k].x, acc0[k].y, acc1[k].x, acc1[k].y);
-        if (p.y_mc | p.y_np) st_y(ya, yv, p);
+        if constexpr (REMOTE) st_y(ya, yv, p);
         else *ya = yv;
       }
   }

@@ -71,7 +71,9 @@ __host__ inline bool apply_tc_supported(int N, int S, int K) { return S == 16 &&
 // k-step two MMAs: Ahi x [Bhi; Blo] (N = 64) into
 // accumulator columns [0,64) and Alo x Bhi (N = 32) into [0,32); the epilogue adds
 // column c and c + 32.
-template <int KS>
+// REMOTE: Y stores go through st_y (multicast / peer copies); the plain instantiation
+// compiles to ordinary stores only.
+template <int KS, bool REMOTE>
 __global__ void __launch_bounds__(kApplyTcThreads, 2)
     apply_tc_kernel(const __grid_constant__ CUtensorMap cube_map, KParams p, const float2* __restrict__ wts,
                     float2* __restrict__ out, int units, int ns) {
@@ -225,8 +227,7 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
         const float o = __shfl_xor_sync(0xffffffffu, b[k] + d[k], 1);  // partner row's Out[.][S+k]
         yv[k] = fmaf(sg, o, re);
       }
-      // the remote-store branch is taken once per tile, outside the store loop
-      if (p.y_mc | p.y_np) {
+      if constexpr (REMOTE) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) st_y(yp + (long long)k * 2 * R, yv[k], p);
       } else {

@@ -1,5 +1,5 @@
 // common.cuh -- device-side parameter block and sm_100a primitives shared by the
-// STAP kernels (cov.cuh, solve.cuh, apply.cuh, fused.cuh).  Product code: this
+// STAP kernels (cov.cuh, chol.cuh, apply.cuh, fused.cuh).  Product code: this
 // file never includes or mirrors anything from oracle/.
 #pragma once
 #include <cuda_runtime.h>

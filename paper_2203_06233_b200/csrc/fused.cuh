@@ -1,7 +1,7 @@
 // fused.cuh -- K4: the whole path in one kernel (stap_run): cube in, Y out,
 // no HBM intermediates.
 //
-// Method: exactly K1 -> K2 -> K3 (cov.cuh, solve.cuh / solve_small.cuh,
+// Method: exactly K1 -> K2 -> K3 (cov.cuh, chol.cuh / solve_small.cuh,
 // apply.cuh) for every unit; the same device functions compute the lag
 // blocks, the loaded covariance and the Cholesky/solves, so a fused unit is
 // computed with the same summation orders as the staged path.
@@ -12,7 +12,8 @@
 //   2. lag-block HERK (cta_lag_blocks) -> scaled blocks in shared memory;
 //   3. delta per bin from the lag-0 blocks;
 //   4. solver segments (a lane group per matrix) take bins round-robin: load the
-//      loaded R straight from the lag blocks into registers, Cholesky + solves,
+//      loaded R straight from the lag blocks into registers, Cholesky + solves
+//      (solve_small.cuh for N <= 16, chol.cuh above),
 //      publish w_k in shared [i][SMAX], then apply the S weights to the K cells
 //      of the bin straight from the window (lane = range cell, S accumulators,
 //      broadcast float4 weight reads) and store Y with coalesced 8-byte stores.
@@ -22,7 +23,7 @@
 #include <cstring>
 
 #include "cov.cuh"
-#include "solve.cuh"
+#include "chol.cuh"
 #include "solve_small.cuh"
 
 namespace stapk {
@@ -65,12 +66,12 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int T, int K, int P, 
 
 // ---- solver policies: load R of bin pr from the lag blocks, solve, publish w in wsm[i][SMAX]
 template <class CF>
-struct GroupSolverPolicy {
+struct CholSolverPolicy {
   static constexpr int G = CF::G;
   static constexpr int kMaxThreads = 256, kMinBlocks = CF::G > 32 ? 1 : 2;
   static constexpr bool kWInShared = false;
   static constexpr int kN = 0;
-  using Shared = SolveShared<CF>;
+  using Shared = CholShared<CF>;
   template <int C, int SMAX>
   __device__ static __forceinline__ int solve_bin(const KParams& p, const float2* blk, int W, int pr, float dlt,
                                                   const float2* __restrict__ steer, Shared& sh, int gl, int bar_id,
@@ -84,8 +85,8 @@ struct GroupSolverPolicy {
 #pragma unroll
       for (int u = CF::umin(v); u < MR; ++u) {
         const int i = PR * u + gp, l = PC * v + gq;
-        float2 x = make_float2(0.f, 0.f);
-        if (i < N && l <= i) {
+        float2 x = make_float2(i == l ? 1.f : 0.f, 0.f);  // identity padding beyond N
+        if (i < N && l < N) {
           x = rhat_from_blocks(blk, C, W, pr, i, l);
           if (i == l) x = make_float2(x.x + dlt, 0.f);
         }
@@ -98,7 +99,8 @@ struct GroupSolverPolicy {
         const int i = PR * u + gp, k = PC * kv + gq;
         B[u][kv] = (i < N && k < S) ? __ldg(steer + k * N + i) : make_float2(0.f, 0.f);
       }
-    const int inf = group_chol_solve<CF>(N, S, A, B, sh, gl, bar_id);
+    float gam[SC];
+    const int inf = chol_solve_group<CF>(N, S, A, B, sh, gl, bar_id, gam);
 #pragma unroll
     for (int u = 0; u < MR; ++u)
 #pragma unroll
@@ -140,7 +142,9 @@ struct SmallSolverPolicy {
   }
 };
 
-template <int C, int SMAX, class SP>
+// REMOTE: Y stores go through st_y (multicast / peer copies); the plain instantiation
+// compiles to ordinary stores only.
+template <int C, int SMAX, class SP, bool REMOTE>
 __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
     fused_kernel(KParams p, const float2* __restrict__ cube, const float2* __restrict__ steer,
                  float2* __restrict__ out, int32_t* __restrict__ info, int P) {
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
 #else
     const int inf = SP::template solve_bin<C, SMAX>(p, blk, W, pr, delta_s[pr], steer, sh, gl, bar_id, wsm);
 #endif
-    group_sync<G>(bar_id);
+    chol_sync<G>(bar_id);
     STAPK_PROF_T(ps1);
     if (gl == 0) STAPK_PROF_ADD(1, ps1 - ps0);
 
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
             }
           }
         }
-        if (p.y_mc | p.y_np) {  // remote stores: branch once per pass, outside the store loop
+        if constexpr (REMOTE) {
 #pragma unroll
           for (int k = 0; k < SMAX; ++k)
             if (k < S) {
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
         }
       }
     }
-    group_sync<G>(bar_id);
+    chol_sync<G>(bar_id);
     STAPK_PROF_T(ps2);
     if (gl == 0) STAPK_PROF_ADD(2, ps2 - ps1);
   }
@@ -272,13 +276,11 @@ __global__ void __launch_bounds__(SP::kMaxThreads, SP::kMinBlocks)
 // (C, SMAX, N, solver) instantiations: the BASELINE.json shapes.
 using FusedSolverTiny = SmallSolverPolicy<4, 16>;
 using FusedSolverSmall = SmallSolverPolicy<12, 16>;
-using FusedSolverMedium = GroupSolverPolicy<SolveCfg16>;
-using FusedSolverLarge = GroupSolverPolicy<SolveCfg22>;
+using FusedSolverMedium = CholSolverPolicy<CholCfg<4, 8, 8, 4, 2, false, 2>>;
 #define STAPK_FUSED_CFGS(X)             \
   X(2, 4, 4, FusedSolverTiny)           \
   X(4, 16, 12, FusedSolverSmall)        \
-  X(6, 16, 30, FusedSolverMedium)       \
-  X(8, 16, 56, FusedSolverLarge)
+  X(6, 16, 30, FusedSolverMedium)
 
 inline int fused_smax(int S) { return S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <= 16 ? 16 : 32; }
 
@@ -305,7 +307,7 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
     bool got = false;
 #define X(CC, SM, NN, SPT)                                                            \
     if (!got && kp.C == CC && SMAX == SM && kp.N == NN)                                \
-      got = cudaFuncGetAttributes(&fa, fused_kernel<CC, SM, SPT>) == cudaSuccess;
+      got = cudaFuncGetAttributes(&fa, fused_kernel<CC, SM, SPT, false>) == cudaSuccess;
     STAPK_FUSED_CFGS(X)
 #undef X
     if (got) regs = fa.numRegs;
@@ -361,9 +363,11 @@ inline bool fused_configure(const KParams& kp, FusedCfg* f) {
 }
 
 inline void fused_set_attr(const FusedCfg& f) {
-#define X(CC, SM, NN, SPT)                                                                                  \
-  if (f.C == CC && f.SMAX == SM && f.N == NN)                                                               \
-    cudaFuncSetAttribute(fused_kernel<CC, SM, SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
+#define X(CC, SM, NN, SPT)                                                                                         \
+  if (f.C == CC && f.SMAX == SM && f.N == NN) {                                                                    \
+    cudaFuncSetAttribute(fused_kernel<CC, SM, SPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem); \
+    cudaFuncSetAttribute(fused_kernel<CC, SM, SPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);  \
+  }
   STAPK_FUSED_CFGS(X)
 #undef X
 }
@@ -371,9 +375,13 @@ inline void fused_set_attr(const FusedCfg& f) {
 inline void fused_launch(const FusedCfg& f, const KParams& kp, const float2* cube, const float2* steer,
                          float2* out, int32_t* info, cudaStream_t st) {
   dim3 grid(f.runs, kp.B, kp.batch);
-#define X(CC, SM, NN, SPT)                         \
-  if (f.C == CC && f.SMAX == SM && f.N == NN)      \
-    fused_kernel<CC, SM, SPT><<<grid, f.threads, f.smem, st>>>(kp, cube, steer, out, info, f.P);
+#define X(CC, SM, NN, SPT)                                                                       \
+  if (f.C == CC && f.SMAX == SM && f.N == NN) {                                                  \
+    if (kp.y_mc | kp.y_np)                                                                       \
+      fused_kernel<CC, SM, SPT, true><<<grid, f.threads, f.smem, st>>>(kp, cube, steer, out, info, f.P); \
+    else                                                                                         \
+      fused_kernel<CC, SM, SPT, false><<<grid, f.threads, f.smem, st>>>(kp, cube, steer, out, info, f.P); \
+  }
   STAPK_FUSED_CFGS(X)
 #undef X
 }

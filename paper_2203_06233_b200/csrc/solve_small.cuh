@@ -1,7 +1,7 @@
 // solve_small.cuh -- K2 for N <= 16: Cholesky + forward/back solves, fully
 // register-resident, compile-time N.
 //
-// Method: as solve.cuh (readings c-9, c-10, c-11).
+// Method: as chol.cuh (readings c-9, c-10, c-11).
 //
 // Layout: a segment of LANES lanes (16 -> two matrices per warp when S <= 16,
 // else 32) owns one matrix.

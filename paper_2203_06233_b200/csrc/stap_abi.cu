@@ -2,7 +2,8 @@
 // selection and the extern "C" entry points declared in include/stap.h.
 //
 // Nothing here does arithmetic of the method; every step runs in the kernels
-// of cov.cuh (K1), solve.cuh (K2), apply.cuh (K3) and fused.cuh (K4).  There
+// of cov.cuh / cov_tc.cuh (K1), chol.cuh / solve_small.cuh (K2), apply.cuh / apply_tc.cuh
+// (K3) and fused.cuh (K4).  There
 // is no CPU path: without an sm_100 device every call returns an error.
 #include <cmath>
 #include <cstdlib>
@@ -13,13 +14,14 @@
 #include <cudaTypedefs.h>
 
 #include "../../include/stap.h"
+#include "internal.h"
 #include "apply.cuh"
 #include "apply_tc.cuh"
 #include "cov.cuh"
 #include "cov_tc.cuh"
 #include "doppler.cuh"
 #include "fused.cuh"
-#include "solve.cuh"
+#include "chol.cuh"
 #include "solve_small.cuh"
 
 using namespace stapk;
@@ -35,9 +37,9 @@ struct stap_plan {
   CovTcGeom cov_tc_geom;
   size_t cov_tc_smem;
   // K2
-  SolveSel solve_sel;
+  CholSel solve_sel;             // N > 16: chol.cuh
   int solve_small, solve_lanes;  // N <= 16: solve_small.cuh with `solve_lanes` lanes per matrix
-  int solve_groups, solve_grid;
+  int solve_grid;
   size_t solve_smem;
   // K3
   int apply_tpu, apply_upc, apply_smax, apply_grid;
@@ -76,6 +78,8 @@ void plan_free(stap_plan* pl) {
 namespace {
 
 const size_t kSmemCap = 227 * 1024;
+// a 16-byte aligned stand-in address for the plan-time tensor-map trial encode (never dereferenced)
+const float2* const kTrialCube = reinterpret_cast<const float2*>(uintptr_t{1} << 20);
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -142,8 +146,13 @@ bool encode_cube_map(const KParams& k, const float2* cube, CUtensorMap* map, int
              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-
-
+// the two tensor maps the tcgen05 stages build per call (any 16-byte aligned cube)
+bool encode_cov_tc_map(const stap_plan* pl, const float2* cube, CUtensorMap* m) {
+  return encode_cube_map(pl->kp, cube, m, 32, pl->cov_tc_geom.MB * pl->kp.C, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+bool encode_apply_tc_map(const stap_plan* pl, const float2* cube, CUtensorMap* m) {
+  return encode_cube_map(pl->kp, cube, m, 128, pl->kp.C);
+}
 
 template <int C>
 void cov_launch_t(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
@@ -151,13 +160,15 @@ void cov_launch_t(const stap_plan* pl, const float2* cube, float2* cov, cudaStre
   cov_kernel<C><<<grid, pl->cov_threads, pl->cov_smem, st>>>(pl->kp, cube, cov, pl->cov_P);
 }
 
-void cov_launch(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
-  CUtensorMap msw;
-  if (pl->cov_tc &&  // (an unaligned cube view takes the SIMT kernel)
-      encode_cube_map(pl->kp, cube, &msw, 32, pl->cov_tc_geom.MB * pl->kp.C, CU_TENSOR_MAP_SWIZZLE_128B)) {
+// K1 on the kernel the plan chose (tcgen05 3xTF32 only under STAP_PREC_TF32X3); a tensor map
+// that cannot be encoded is an error, never a silent switch of arithmetic.
+stap_status cov_launch(const stap_plan* pl, const float2* cube, float2* cov, cudaStream_t st) {
+  if (pl->cov_tc) {
+    CUtensorMap msw;
+    if (!encode_cov_tc_map(pl, cube, &msw)) return STAP_ERR_CUDA;
     cov_tc_kernel<<<pl->cov_tc_grid, kCovTcThreads, pl->cov_tc_smem, st>>>(msw, pl->kp, cube, cov, pl->cov_tc_tiles,
                                                                            pl->cov_tc_geom);
-    return;
+    return STAP_OK;
   }
   switch (pl->kp.C) {
     case 1: cov_launch_t<1>(pl, cube, cov, st); break;
@@ -169,59 +180,84 @@ void cov_launch(const stap_plan* pl, const float2* cube, float2* cov, cudaStream
     case 7: cov_launch_t<7>(pl, cube, cov, st); break;
     case 8: cov_launch_t<8>(pl, cube, cov, st); break;
   }
+  return STAP_OK;
 }
 
-template <int SMAX>
+// K3 instantiations: SIMT by SMAX, tcgen05 by KS = ceil(N/8); each plain or REMOTE (multicast /
+// peer-copy stores), the plain ones compiled with ordinary stores only
+template <int SMAX, bool RM>
 void apply_launch_t(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
-  apply_kernel<SMAX><<<pl->apply_grid, pl->apply_upc * pl->apply_tpu, pl->apply_smem, st>>>(
+  apply_kernel<SMAX, RM><<<pl->apply_grid, pl->apply_upc * pl->apply_tpu, pl->apply_smem, st>>>(
       pl->kp, cube, w, out, pl->apply_tpu, pl->apply_upc, pl->units);
 }
-
-template <int KS>
+template <int KS, bool RM>
 void apply_tc_launch_t(const stap_plan* pl, const CUtensorMap& map, const float2* w, float2* out, cudaStream_t st) {
-  apply_tc_kernel<KS><<<pl->apply_tc_grid, kApplyTcThreads, pl->apply_tc_smem, st>>>(map, pl->kp, w, out,
-                                                                                      (int)pl->units, pl->apply_tc_ns);
+  apply_tc_kernel<KS, RM><<<pl->apply_tc_grid, kApplyTcThreads, pl->apply_tc_smem, st>>>(map, pl->kp, w, out,
+                                                                                          (int)pl->units, pl->apply_tc_ns);
+}
+template <bool RM>
+void apply_tc_dispatch(const stap_plan* pl, const CUtensorMap& map, const float2* w, float2* out, cudaStream_t st) {
+  switch ((pl->kp.N + 7) / 8) {
+    case 1: apply_tc_launch_t<1, RM>(pl, map, w, out, st); break;
+    case 2: apply_tc_launch_t<2, RM>(pl, map, w, out, st); break;
+    case 3: apply_tc_launch_t<3, RM>(pl, map, w, out, st); break;
+    case 4: apply_tc_launch_t<4, RM>(pl, map, w, out, st); break;
+    case 5: apply_tc_launch_t<5, RM>(pl, map, w, out, st); break;
+    case 6: apply_tc_launch_t<6, RM>(pl, map, w, out, st); break;
+    case 7: apply_tc_launch_t<7, RM>(pl, map, w, out, st); break;
+    case 8: apply_tc_launch_t<8, RM>(pl, map, w, out, st); break;
+  }
+}
+template <bool RM>
+void apply_simt_dispatch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
+  switch (pl->apply_smax) {
+    case 2: apply_launch_t<2, RM>(pl, cube, w, out, st); break;
+    case 4: apply_launch_t<4, RM>(pl, cube, w, out, st); break;
+    case 8: apply_launch_t<8, RM>(pl, cube, w, out, st); break;
+    case 16: apply_launch_t<16, RM>(pl, cube, w, out, st); break;
+    case 32: apply_launch_t<32, RM>(pl, cube, w, out, st); break;
+  }
+}
+template <int KS>
+void apply_tc_attr_t(size_t smem) {
+  cudaFuncSetAttribute(apply_tc_kernel<KS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(apply_tc_kernel<KS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 void apply_tc_attr(int N, size_t smem) {
   switch ((N + 7) / 8) {
-    case 1: cudaFuncSetAttribute(apply_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 2: cudaFuncSetAttribute(apply_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 3: cudaFuncSetAttribute(apply_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 4: cudaFuncSetAttribute(apply_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 5: cudaFuncSetAttribute(apply_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 6: cudaFuncSetAttribute(apply_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 7: cudaFuncSetAttribute(apply_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 8: cudaFuncSetAttribute(apply_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 1: apply_tc_attr_t<1>(smem); break;
+    case 2: apply_tc_attr_t<2>(smem); break;
+    case 3: apply_tc_attr_t<3>(smem); break;
+    case 4: apply_tc_attr_t<4>(smem); break;
+    case 5: apply_tc_attr_t<5>(smem); break;
+    case 6: apply_tc_attr_t<6>(smem); break;
+    case 7: apply_tc_attr_t<7>(smem); break;
+    case 8: apply_tc_attr_t<8>(smem); break;
   }
 }
 
-void apply_launch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
-  CUtensorMap map;
-  if (pl->apply_tc && encode_cube_map(pl->kp, cube, &map, 128, pl->kp.C)) {  // (an unaligned cube view takes the SIMT kernel)
-    switch ((pl->kp.N + 7) / 8) {
-      case 1: apply_tc_launch_t<1>(pl, map, w, out, st); break;
-      case 2: apply_tc_launch_t<2>(pl, map, w, out, st); break;
-      case 3: apply_tc_launch_t<3>(pl, map, w, out, st); break;
-      case 4: apply_tc_launch_t<4>(pl, map, w, out, st); break;
-      case 5: apply_tc_launch_t<5>(pl, map, w, out, st); break;
-      case 6: apply_tc_launch_t<6>(pl, map, w, out, st); break;
-      case 7: apply_tc_launch_t<7>(pl, map, w, out, st); break;
-      case 8: apply_tc_launch_t<8>(pl, map, w, out, st); break;
-    }
-    return;
+stap_status apply_launch(const stap_plan* pl, const float2* cube, const float2* w, float2* out, cudaStream_t st) {
+  const bool rm = pl->kp.y_mc || pl->kp.y_np;
+  if (pl->apply_tc) {
+    CUtensorMap map;
+    if (!encode_apply_tc_map(pl, cube, &map)) return STAP_ERR_CUDA;
+    if (rm)
+      apply_tc_dispatch<true>(pl, map, w, out, st);
+    else
+      apply_tc_dispatch<false>(pl, map, w, out, st);
+    return STAP_OK;
   }
-  switch (pl->apply_smax) {
-    case 2: apply_launch_t<2>(pl, cube, w, out, st); break;
-    case 4: apply_launch_t<4>(pl, cube, w, out, st); break;
-    case 8: apply_launch_t<8>(pl, cube, w, out, st); break;
-    case 16: apply_launch_t<16>(pl, cube, w, out, st); break;
-    case 32: apply_launch_t<32>(pl, cube, w, out, st); break;
-  }
+  if (rm)
+    apply_simt_dispatch<true>(pl, cube, w, out, st);
+  else
+    apply_simt_dispatch<false>(pl, cube, w, out, st);
+  return STAP_OK;
 }
 
 template <int SMAX>
 void apply_attr(size_t smem) {
-  cudaFuncSetAttribute(apply_kernel<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(apply_kernel<SMAX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(apply_kernel<SMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 void set_apply_attr(int smax, size_t smem) {
@@ -240,8 +276,7 @@ void solve_dispatch(const stap_plan* pl, const float2* cov, const float2* steer,
     solve_small_launch(pl->kp.N, pl->solve_lanes, pl->solve_grid, 256, pl->solve_smem, st, pl->kp.S, pl->units, cov,
                        steer, w, g, info);
   else
-    solve_launch(pl->solve_sel, pl->solve_grid, pl->solve_groups * pl->solve_sel.G, pl->solve_smem, st, pl->kp.N,
-                 pl->kp.S, pl->units, cov, steer, w, g, info);
+    chol_launch(pl->solve_sel, pl->solve_grid, st, pl->kp.N, pl->kp.S, pl->units, cov, steer, w, g, info);
 }
 
 stap_status check_launch() {
@@ -259,13 +294,28 @@ stap_status staged_run(const stap_plan* pl, const float2* cube, const float2* st
   float2* cov = reinterpret_cast<float2*>(w);
   float2* wts = reinterpret_cast<float2*>(w + pl->ws_cov);
   float* gam = reinterpret_cast<float*>(w + pl->ws_cov + pl->ws_w);
-  cov_launch(pl, cube, cov, st);
+  stap_status s = cov_launch(pl, cube, cov, st);
+  if (s != STAP_OK) return s;
   solve_dispatch(pl, cov, steer, wts, gam, info, st);
-  apply_launch(pl, cube, wts, out, st);
+  s = apply_launch(pl, cube, wts, out, st);
+  if (s != STAP_OK) return s;
   return check_launch();
 }
 
 }  // namespace
+
+namespace stapk {
+bool plan_out_geom(const stap_plan* pl, PlanOutGeom* g) {
+  if (!pl || !g) return false;
+  g->batch = pl->prm.batch;
+  g->dop_count = pl->prm.dop_count;
+  g->S = pl->prm.n_steering;
+  g->R = pl->prm.n_range;
+  g->device = pl->prm.device;
+  g->out_bytes = pl->out_bytes;
+  return true;
+}
+}  // namespace stapk
 
 extern "C" {
 
@@ -286,6 +336,7 @@ const char* stap_status_string(stap_status s) {
     case STAP_ERR_UNSUPPORTED: return "STAP_ERR_UNSUPPORTED: valid but not implemented (N>64, S>32, C>8, odd K, window > smem)";
     case STAP_ERR_MISALIGNED: return "STAP_ERR_MISALIGNED: device pointer not 16-byte aligned";
     case STAP_ERR_CUDA: return "STAP_ERR_CUDA: CUDA runtime or launch error";
+    case STAP_ERR_NCCL: return "STAP_ERR_NCCL: NCCL unavailable, or an NCCL / IPC call failed";
     case STAP_ERR_DEVICE: return "STAP_ERR_DEVICE: no sm_100 device at the plan's ordinal";
   }
   return "STAP_ERR_UNKNOWN";
@@ -302,6 +353,7 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
             S = p->n_steering;
   if (C <= 0 || T <= 0 || D <= 0 || R <= 0 || K <= 0 || S <= 0 || p->batch <= 0) return STAP_ERR_BAD_DIMS;
   if (p->path < STAP_PATH_AUTO || p->path > STAP_PATH_STAGED) return STAP_ERR_BAD_DIMS;
+  if (p->precision != STAP_PREC_FP32 && p->precision != STAP_PREC_TF32X3) return STAP_ERR_BAD_DIMS;
   if (p->out_multicast != 0 && p->out_multicast != 1) return STAP_ERR_BAD_DIMS;
   if (p->out_n_peers < 0 || p->out_n_peers > 7 || (p->out_n_peers > 0 && p->out_multicast)) return STAP_ERR_BAD_DIMS;
   for (int i = 0; i < p->out_n_peers; ++i)
@@ -364,41 +416,48 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   pl->cov_runs = (p->dop_count + P - 1) / P;
   pl->cov_smem = cov_smem_bytes(C, T, K, P);
   {
-    const char* e = getenv("STAP_COV_SIMT");  // developer A/B knob
+    // tcgen05 3xTF32 covariance only when the caller asked for it (stap_params.precision) and the
+    // shape and a trial tensor-map encode allow it; decided here, once, for every call of the plan
     pl->cov_tc_geom = cov_tc_geom(C, T, N, p->dop_count);
     pl->cov_tc_tiles = p->batch * kp.B * pl->cov_tc_geom.ntd;
     pl->cov_tc_smem = cov_tc_smem(N, pl->cov_tc_geom.RS, pl->cov_tc_geom.OB).total;
-    pl->cov_tc = (cov_tc_supported(C, T, N, K) && tensor_map_encoder() && pl->cov_tc_smem <= kSmemCap &&
-                  !(e && atoi(e)))
+    pl->cov_tc = (p->precision == STAP_PREC_TF32X3 && cov_tc_supported(C, T, N, K) && tensor_map_encoder() &&
+                  pl->cov_tc_smem <= kSmemCap)
                      ? 1
                      : 0;
+    CUtensorMap trial;
+    if (pl->cov_tc && !encode_cov_tc_map(pl, kTrialCube, &trial)) pl->cov_tc = 0;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
     pl->cov_tc_grid = pl->cov_tc_tiles < nsm ? pl->cov_tc_tiles : nsm;  // persistent, one CTA per SM
   }
 
-  // K2: lane-group layout for (N, S); 256 threads per CTA
-  if (!solve_select(N, S, &pl->solve_sel)) {
-    delete pl;
-    return STAP_ERR_UNSUPPORTED;
-  }
-  pl->solve_groups = 256 / pl->solve_sel.G;
-  pl->solve_smem = solve_smem_bytes(pl->solve_sel, pl->solve_groups, N, S);
-  if (pl->solve_smem > kSmemCap) {
-    delete pl;
-    return STAP_ERR_UNSUPPORTED;
-  }
-  {
-    long long sg = (pl->units + pl->solve_groups - 1) / pl->solve_groups;
-    pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
-  }
+  // K2: N <= 16 -> solve_small (two matrices per warp for S <= 16); else chol.cuh's lane-group
+  // layout for (N, S).  Persistent grids: the blocks resident on every SM.
   pl->solve_small = N <= 16;
-  if (pl->solve_small) {
-    pl->solve_lanes = S <= 16 ? 16 : 32;
-    const int per_cta = 8 * (32 / pl->solve_lanes);  // matrices per 256-thread CTA
-    pl->solve_smem = solve_small_smem(N, pl->solve_lanes, 256);
-    long long sg = (pl->units + per_cta - 1) / per_cta;
-    pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+    if (pl->solve_small) {
+      pl->solve_lanes = S <= 16 ? 16 : 32;
+      const int per_cta = 8 * (32 / pl->solve_lanes);  // matrices per 256-thread CTA
+      pl->solve_smem = solve_small_smem(N, pl->solve_lanes, 256);
+      long long sg = (pl->units + per_cta - 1) / per_cta;
+      pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
+    } else {
+      if (!chol_select(N, S, &pl->solve_sel)) {
+        delete pl;
+        return STAP_ERR_UNSUPPORTED;
+      }
+      pl->solve_smem = pl->solve_sel.smem;
+      const long long sg = (pl->units + pl->solve_sel.groups - 1) / pl->solve_sel.groups;
+      const long long cap = (long long)nsm * pl->solve_sel.min_blocks;
+      pl->solve_grid = (int)(sg < cap ? sg : cap);
+    }
+    if (pl->solve_smem > kSmemCap) {
+      delete pl;
+      return STAP_ERR_UNSUPPORTED;
+    }
   }
 
   // K3
@@ -408,9 +467,12 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   pl->apply_smem = apply_smem_bytes(N, pl->apply_smax, pl->apply_upc);
   pl->apply_grid = (int)((pl->units + pl->apply_upc - 1) / pl->apply_upc);
   {
-    const char* e = getenv("STAP_APPLY_SIMT");  // developer A/B knob
-    pl->apply_tc =
-        (apply_tc_supported(N, S, K) && pl->units < (1LL << 30) && tensor_map_encoder() && !(e && atoi(e))) ? 1 : 0;
+    pl->apply_tc = (p->precision == STAP_PREC_TF32X3 && apply_tc_supported(N, S, K) && pl->units < (1LL << 30) &&
+                    tensor_map_encoder())
+                       ? 1
+                       : 0;
+    CUtensorMap trial;
+    if (pl->apply_tc && !encode_apply_tc_map(pl, kTrialCube, &trial)) pl->apply_tc = 0;
     pl->apply_tc_ns = apply_tc_stages(N);
     pl->apply_tc_smem = apply_tc_smem_bytes(N);
     int nsm = 148;
@@ -458,7 +520,7 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
     if (pl->solve_small)
       solve_small_set_attr(N, pl->solve_lanes, pl->solve_smem);
     else
-      solve_set_attr(pl->solve_sel, pl->solve_smem);
+      chol_set_attr(pl->solve_sel);
     set_apply_attr(pl->apply_smax, pl->apply_smem);
     if (pl->apply_tc)
       apply_tc_attr(N, pl->apply_tc_smem);
@@ -473,7 +535,7 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   else
     snprintf(pl->desc, sizeof pl->desc, "staged:cov(%s,P=%d,thr=%d,smem=%zu)+solve(id=%d,G=%d)+apply(%s,tpu=%d,upc=%d)",
              pl->cov_tc ? "tcgen05-3xtf32" : "simt", pl->cov_P, pl->cov_threads, pl->cov_smem, pl->solve_small ? 100 + N : pl->solve_sel.id,
-             pl->solve_small ? pl->solve_lanes : pl->solve_sel.G, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
+             pl->solve_small ? pl->solve_lanes : pl->solve_sel.threads / pl->solve_sel.groups, pl->apply_tc ? "tcgen05-3xtf32" : "simt", pl->apply_tpu,
              pl->apply_upc);
   // host-I/O pipelining (stap_run_host): up to 8 equal chunks of whole cubes.  A chunk count
   // whose per-chunk buffers would not keep 16-byte offsets is skipped (e.g. an odd number of
@@ -587,7 +649,8 @@ stap_status stap_covariance(const stap_plan* pl, const stap_c64* cube, stap_c64*
   if (!aligned16(cube) || !aligned16(cov)) return STAP_ERR_MISALIGNED;
   DeviceGuard g(pl->prm.device);
   if (!g.ok) return STAP_ERR_DEVICE;
-  cov_launch(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<float2*>(cov), st);
+  const stap_status s = cov_launch(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<float2*>(cov), st);
+  if (s != STAP_OK) return s;
   return check_launch();
 }
 
@@ -610,8 +673,9 @@ stap_status stap_apply(const stap_plan* pl, const stap_c64* cube, const stap_c64
   if (!aligned16(cube) || !aligned16(weights) || !aligned16(out)) return STAP_ERR_MISALIGNED;
   DeviceGuard g(pl->prm.device);
   if (!g.ok) return STAP_ERR_DEVICE;
-  apply_launch(pl, reinterpret_cast<const float2*>(cube), reinterpret_cast<const float2*>(weights),
-               reinterpret_cast<float2*>(out), st);
+  const stap_status s = apply_launch(pl, reinterpret_cast<const float2*>(cube),
+                                     reinterpret_cast<const float2*>(weights), reinterpret_cast<float2*>(out), st);
+  if (s != STAP_OK) return s;
   return check_launch();
 }
 
@@ -685,7 +749,10 @@ stap_status stap_run_host(const stap_plan* pl, const stap_c64* h_cube, const sta
   }
   if (cudaMemcpyAsync(d_cube, h_cube, pl->cube_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(d_steer, h_steering, pl->steer_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return check_launch() == STAP_OK ? STAP_ERR_CUDA : STAP_ERR_CUDA;
+  {
+    cudaGetLastError();
+    return STAP_ERR_CUDA;
+  }
   stap_status s = stap_run(pl, reinterpret_cast<const stap_c64*>(d_cube), reinterpret_cast<const stap_c64*>(d_steer),
                            reinterpret_cast<stap_c64*>(d_out), reinterpret_cast<int32_t*>(d_info), workspace,
                            pl->ws_total, st);

@@ -33,8 +33,8 @@ def test_header_symbols_exported(pkg):
 
 
 def test_abi_version_and_strings(pkg):
-    assert pkg.stap_abi_version() == 3
-    for code in (0, 1, 2, 3, 4, 5, 7):
+    assert pkg.stap_abi_version() == 4
+    for code in (0, 1, 2, 3, 4, 5, 6, 7):
         assert pkg.stap_status_string(code).startswith(pkg.STATUS[code])
 
 
@@ -68,6 +68,7 @@ def _params(pkg, **kw):
     (dict(out_multicast=2), 2), (dict(out_multicast=-1), 2),    # not 0 or 1 (ABI v3)
     (dict(out_n_peers=8), 2), (dict(out_n_peers=-1), 2), (dict(out_n_peers=1, out_multicast=1), 2),
     (dict(out_n_peers=1, out_peer_offset=(ctypes.c_int64 * 7)(8)), 4),  # offset not a multiple of 16
+    (dict(precision=2), 2), (dict(precision=-1), 2),             # not a stap_precision (ABI v4)
     (dict(n_chan=9, tdof=7), 3), (dict(n_steering=33), 3),
     (dict(training_block=7, n_range=511), 3), (dict(n_chan=8, tdof=9), 3),
 ])
@@ -86,6 +87,19 @@ def test_null_args(pkg):
     assert pkg._lib.stap_covariance(None, None, None, None) == 1
     assert pkg._lib.stap_doppler(None, None, None, None, None) == 1
     assert pkg._lib.stap_plan_destroy(None) == 0
+
+
+def test_comm_null_args(pkg):
+    """The multi-GPU extension validates its arguments before touching NCCL or a device."""
+    h = ctypes.c_void_p()
+    assert pkg._lib.stap_comm_create(2, None, ctypes.byref(h)) == 1
+    assert pkg._lib.stap_comm_create(0, (ctypes.c_int32 * 1)(0), ctypes.byref(h)) == 2
+    assert pkg._lib.stap_comm_init_rank(2, 0, None, 0, ctypes.byref(h)) == 1
+    assert pkg._lib.stap_comm_init_rank(2, 2, b"\0" * 128, 0, ctypes.byref(h)) == 2
+    assert pkg._lib.stap_comm_unique_id(None) == 1
+    assert pkg._lib.stap_comm_allgather_out(None, None, None, None) == 1
+    assert pkg._lib.stap_comm_peer_offsets(None, None, None, None) == 1
+    assert pkg._lib.stap_comm_destroy(None) == 0
 
 
 def test_no_device_no_fallback(pkg):

@@ -68,9 +68,10 @@ def run_gpu(stap, cfg, cube, st, staged=False, **kw):
 
 
 # ---------------------------------------------------------------- whole path vs oracle
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("name", ["tiny", "small", "medium"])
 @pytest.mark.parametrize("mode", ["run-auto", "run-fused", "run-staged", "stages"])
-def test_run_vs_oracle_full(stap, name, mode):
+def test_run_vs_oracle_full(stap, name, mode, prec):
     cfg = synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "ula" if name != "tiny" else "random")
@@ -79,9 +80,9 @@ def test_run_vs_oracle_full(stap, name, mode):
     path = mode[4:] if mode.startswith("run-") else "auto"
     if name == "tiny" and path == "fused":  # below the fused kernel's occupancy floor
         with pytest.raises(stap.StapError):
-            plan_for(stap, cfg, path="fused")
+            plan_for(stap, cfg, path="fused", precision=prec)
         return
-    res = run_gpu(stap, cfg, cube, st, staged=staged, path=path)
+    res = run_gpu(stap, cfg, cube, st, staged=staged, path=path, precision=prec)
     assert res[0].description.startswith({"fused": "fused", "staged": "staged"}.get(path, ""))
     Y, info = res[1][0], res[2][0]
     err = rel_lines(Y, ref["Y"])
@@ -89,26 +90,74 @@ def test_run_vs_oracle_full(stap, name, mode):
     assert err.max() <= 1e-3, (name, staged, err.max(), res[0].description)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("name", ["medium", "large"])
-def test_run_full_size_sampled(stap, name):
-    """Full BASELINE size on the GPU in the bench's launch configuration; the oracle
-    computes sampled Doppler bins one by one (edges + interior) from windowed buffers."""
+def test_run_full_size_every_bin(stap, name, prec):
+    """Full BASELINE size on the GPU in the bench's launch configuration (AUTO path, the
+    bench's batch of distinct cubes) against the oracle on EVERY Doppler bin, block and
+    steering vector of cube 0 (OpenMP over bins; ~10-30 s of host time at large)."""
     cfg = synth.CONFIGS[name]
-    cube = synth.datacube(cfg)
+    M = {"medium": 16, "large": 2}[name]
+    cubes = np.stack([synth.datacube(cfg, i) for i in range(M)])
     st = synth.steering(cfg, "ula")
-    plan, Y, info = run_gpu(stap, cfg, cube, st)
-    for d in (0, 1, cfg.D // 2, cfg.D - 1):
+    plan, Y, info = run_gpu(stap, cfg, cubes, st, batch=M, precision=prec)
+    assert ("tcgen05" in plan.description) == (prec == "tf32x3"), plan.description
+    ref = oracle.run(OP(cfg), cubes[0], st, nthreads=NT)
+    err = rel_lines(Y[0], ref["Y"])
+    assert np.array_equal(info[0], ref["info"])
+    assert err.max() <= 1e-3, (name, err.max(), plan.description)
+    # the last cube of the batch too, on sampled bins (edges + interior)
+    for d in (0, cfg.D // 3, cfg.D - 1):
         b0, nb = synth.shard_window(cfg, d, 1)
-        local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
-        ref = oracle.run(OP(cfg, dop_begin=d, dop_count=1, cube_bin0=b0, cube_bins=nb), local, st, nthreads=NT)
-        err = rel_lines(Y[0, d], ref["Y"][0])
-        assert np.array_equal(info[0, d], ref["info"][0])
-        assert err.max() <= 1e-3, (name, d, err.max(), plan.description)
+        local = np.ascontiguousarray(cubes[M - 1][(b0 + np.arange(nb)) % cfg.D])
+        r1 = oracle.run(OP(cfg, dop_begin=d, dop_count=1, cube_bin0=b0, cube_bins=nb), local, st, nthreads=NT)
+        assert np.array_equal(info[M - 1, d], r1["info"][0])
+        assert rel_lines(Y[M - 1, d], r1["Y"][0]).max() <= 1e-3, (name, d)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_weak_shard_plan_as_bench_builds_it(stap, G):
+    """The exact weak-scaling shard plans bench.py builds at --gpus G (BASELINE configs[4]):
+    global D = 1024*G large cube, rank g owns [1024 g, 1024 (g+1)) from a buffer holding its
+    bins plus the T-1 halo (wrapped at ranks 0 and G-1), batch 2.  Every rank's Y equals the
+    unsharded run over the whole global cube bitwise (P15), and sampled bins at the shard
+    edges match the oracle.  Random device data: the check is the shard mechanics."""
+    import bench
+    base = synth.CONFIGS["large"]
+    gcfg = base.with_(D=base.D * G)
+    M = 2
+    gen = torch.Generator(device="cuda:0").manual_seed(100 + G)
+    full = torch.randn((M, gcfg.D, gcfg.C, gcfg.R), dtype=torch.complex64, device="cuda:0", generator=gen)
+    st = dev(synth.steering(base, "ula"))
+    pf = plan_for(stap, gcfg, batch=M, precision="tf32x3")
+    Yf, If = pf.run(full, st)
+    torch.cuda.synchronize()
+    for g in range(G):
+        lo, cnt = g * base.D, base.D
+        b0, nb = synth.shard_window(gcfg, lo, cnt)
+        idx = torch.from_numpy((b0 + np.arange(nb)) % gcfg.D).cuda(0)
+        local = full.index_select(1, idx).contiguous()
+        ps = plan_for(stap, gcfg, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
+                      precision="tf32x3")
+        assert ps.description == pf.description
+        assert bench.plan_shape_out(stap, ps.dims, lo, cnt, b0, nb, M) == ps.out_shape
+        Ys, Is = ps.run(local, st)
+        torch.cuda.synchronize()
+        assert torch.equal(Ys, Yf[:, lo:lo + cnt]) and torch.equal(Is, If[:, lo:lo + cnt]), g
+        if g in (0, G - 1):
+            xl = local[0].cpu().numpy()
+            for d in (lo, lo + cnt - 1):
+                ob0, onb = synth.shard_window(gcfg, d, 1)
+                rows = [(a - b0) % gcfg.D for a in (ob0 + np.arange(onb))]
+                r1 = oracle.run(OP(gcfg, dop_begin=d, dop_count=1, cube_bin0=ob0, cube_bins=onb),
+                                np.ascontiguousarray(xl[rows]), st.cpu().numpy(), nthreads=NT)
+                assert rel_lines(Ys[0, d - lo].cpu().numpy(), r1["Y"][0]).max() <= 1e-3, (g, d)
 
 
 # ---------------------------------------------------------------- stages vs oracle
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("name", ["tiny", "small", "medium"])
-def test_covariance_vs_oracle(stap, name):
+def test_covariance_vs_oracle(stap, name, prec):
     cfg = synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     if name == "medium":
@@ -116,7 +165,7 @@ def test_covariance_vs_oracle(stap, name):
         Rref, _ = oracle.covariance(OP(cfg2, dop_begin=0, dop_count=24), cube)
     else:
         Rref, _ = oracle.covariance(OP(cfg), cube)
-    plan = plan_for(stap, cfg)
+    plan = plan_for(stap, cfg, precision=prec)
     cov = plan.covariance(dev(cube).reshape(plan.cube_shape)).cpu().numpy()[0]
     cov = cov[:Rref.shape[0]]
     num = np.linalg.norm((cov - Rref).reshape(cov.shape[0], cfg.B, -1), axis=-1)
@@ -132,7 +181,7 @@ def test_covariance_large_tc_vs_oracle(stap):
     cfg = synth.CONFIGS["large"].with_(D=40, R=1024)
     cube = synth.datacube(cfg)
     Rref, _ = oracle.covariance(OP(cfg), cube)
-    plan = plan_for(stap, cfg, path="staged")
+    plan = plan_for(stap, cfg, path="staged", precision="tf32x3")
     assert "cov(tcgen05" in plan.description
     cov = plan.covariance(dev(cube).reshape(plan.cube_shape)).cpu().numpy()[0]
     num = np.linalg.norm((cov - Rref).reshape(cfg.D, cfg.B, -1), axis=-1)
@@ -152,7 +201,7 @@ def test_tensor_core_path_vs_oracle_lambda(stap, name, lam):
         cfg = cfg.with_(R=1024)
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "ula")
-    plan = plan_for(stap, cfg, path="staged")
+    plan = plan_for(stap, cfg, path="staged", precision="tf32x3")
     assert "cov(tcgen05" in plan.description and "apply(tcgen05" in plan.description
     ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
     y, info = plan.run(dev(cube).reshape(plan.cube_shape), dev(st))
@@ -161,14 +210,14 @@ def test_tensor_core_path_vs_oracle_lambda(stap, name, lam):
     assert rel_lines(Y, ref["Y"]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("name", ["small", "medium"])
-def test_covariance_batch_bitwise(stap, name):
+@pytest.mark.parametrize("name,prec", [("small", "fp32"), ("medium", "fp32"), ("medium", "tf32x3")])
+def test_covariance_batch_bitwise(stap, name, prec):
     """A batched covariance equals each cube's own (every tile of every cube, incl. wrapped ones)."""
     cfg = synth.CONFIGS[name]
     M = 6
     xs = np.stack([synth.datacube(cfg, i) for i in range(M)])
-    pb = plan_for(stap, cfg, batch=M, path="staged")
-    p1 = plan_for(stap, cfg, path="staged")
+    pb = plan_for(stap, cfg, batch=M, path="staged", precision=prec)
+    p1 = plan_for(stap, cfg, path="staged", precision=prec)
     cb = pb.covariance(dev(xs).reshape(pb.cube_shape)).cpu().numpy()
     for n in range(M):
         c1 = p1.covariance(dev(xs[n:n + 1]).reshape(p1.cube_shape)).cpu().numpy()[0]
@@ -200,15 +249,16 @@ def test_solve_vs_oracle(stap, name):
     assert np.abs(resp - 1).max() <= 1e-4
 
 
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
-def test_apply_vs_oracle(stap, name):
+def test_apply_vs_oracle(stap, name, prec):
     cfg = synth.CONFIGS[name]
     sub = cfg.with_(D=min(cfg.D, 8) if cfg.D > 8 else cfg.D)
     cube = synth.datacube(sub)
     rng = np.random.default_rng(1)
     W = (rng.standard_normal((sub.D, sub.B, sub.S, sub.N)) + 1j * rng.standard_normal((sub.D, sub.B, sub.S, sub.N))
          ).astype(np.complex64)
-    plan = plan_for(stap, sub)
+    plan = plan_for(stap, sub, precision=prec)
     y = plan.apply(dev(cube).reshape(plan.cube_shape), dev(W).reshape(plan.weights_shape)).cpu().numpy()[0]
     Yr = oracle.apply(OP(sub), cube, W)
     assert rel_lines(y, Yr).max() <= 1e-5
@@ -245,17 +295,23 @@ def test_E3_target_gpu(stap):
         assert abs(Y[0, d, k, r] - alpha) <= 1e-4 * abs(alpha)
 
 
-def test_path_fused_unsupported(stap):
-    """path=fused on a shape the fused kernel cannot hold is STAP_ERR_UNSUPPORTED; auto picks staged."""
+def test_path_and_precision_selection(stap):
+    """path=fused on a shape the fused kernel cannot hold is STAP_ERR_UNSUPPORTED; AUTO picks
+    staged there.  The tensor-core stages run only under precision=tf32x3 (explicit opt-in)."""
     cfg = synth.CONFIGS["large"]
     with pytest.raises(stap.StapError) as e:
         plan_for(stap, cfg, path="fused")
     assert e.value.code == 3
-    assert plan_for(stap, cfg).description.startswith("staged")
-    dm = plan_for(stap, synth.CONFIGS["medium"]).description
+    dl = plan_for(stap, cfg).description
+    assert dl.startswith("staged") and "tcgen05" not in dl, dl
+    dl = plan_for(stap, cfg, precision="tf32x3").description
+    assert dl.startswith("staged") and "cov(tcgen05" in dl and "apply(tcgen05" in dl, dl
+    dm = plan_for(stap, synth.CONFIGS["medium"], precision="tf32x3").description
     assert dm.startswith("staged") and "cov(tcgen05" in dm and "apply(tcgen05" in dm
+    assert "tcgen05" not in plan_for(stap, synth.CONFIGS["medium"], path="staged").description
     assert plan_for(stap, synth.CONFIGS["medium"], path="fused").description.startswith("fused")
     assert plan_for(stap, synth.CONFIGS["small"]).description.startswith("fused")
+    assert plan_for(stap, synth.CONFIGS["small"], precision="tf32x3").description.startswith("fused")
 
 
 # ---------------------------------------------------------------- composition, shards, batch, determinism
@@ -266,14 +322,8 @@ def test_fused_equals_staged(stap, name):
     st = synth.steering(cfg, "ula")
     pf, Yf, If = run_gpu(stap, cfg, cube, st, path="fused")
     assert pf.description.startswith("fused")
-    # same arithmetic: the staged path with the SIMT covariance and apply (developer knobs)
-    os.environ["STAP_COV_SIMT"] = "1"
-    os.environ["STAP_APPLY_SIMT"] = "1"
-    try:
-        res = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
-    finally:
-        del os.environ["STAP_COV_SIMT"]
-        del os.environ["STAP_APPLY_SIMT"]
+    # same arithmetic: the staged path at the default FP32 precision (SIMT covariance and apply)
+    res = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
     assert "cov(simt" in res[0].description and "apply(simt" in res[0].description
     assert np.array_equal(If, res[2])
     e = rel_lines(Yf, res[1]).max()
@@ -281,23 +331,25 @@ def test_fused_equals_staged(stap, name):
     # the default staged path (tcgen05 3xTF32 covariance and apply where they apply) agrees
     # within the oracle tolerance: R differs by <= ~2e-6 relative, amplified at most by
     # the loaded condition number (<= N / lambda); the apply adds <= ~1e-6 per line
-    res2 = run_gpu(stap, cfg, cube, st, staged=True, path="staged")
+    res2 = run_gpu(stap, cfg, cube, st, staged=True, path="staged", precision="tf32x3")
     assert np.array_equal(If, res2[2])
     assert rel_lines(Yf, res2[1]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("name,G", [("tiny", 3), ("small", 2), ("small", 8), ("medium", 4)])
-def test_doppler_shards_bitwise(stap, name, G):
+@pytest.mark.parametrize("name,G,prec", [("tiny", 3, "fp32"), ("small", 2, "fp32"), ("small", 8, "fp32"),
+                                         ("medium", 4, "fp32"), ("medium", 4, "tf32x3")])
+def test_doppler_shards_bitwise(stap, name, G, prec):
     """P15: every shard plan on a slice+halo buffer reproduces the full run bitwise."""
     cfg = synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "ula")
-    _, Yfull, Ifull = run_gpu(stap, cfg, cube, st)
+    _, Yfull, Ifull = run_gpu(stap, cfg, cube, st, precision=prec)
     for g in range(G):
         lo, cnt = synth.shard_range(cfg.D, G, g)
         b0, nb = synth.shard_window(cfg, lo, cnt)
         local = np.ascontiguousarray(cube[(b0 + np.arange(nb)) % cfg.D])
-        _, Y, I = run_gpu(stap, cfg, local, st, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb)
+        _, Y, I = run_gpu(stap, cfg, local, st, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb,
+                          precision=prec)
         assert np.array_equal(Y[0], Yfull[0, lo:lo + cnt])
         assert np.array_equal(I[0], Ifull[0, lo:lo + cnt])
 
@@ -386,26 +438,27 @@ def test_run_host_pipelined_batch(stap, name, M):
     dict(C=5, T=5, D=67, R=64, K=64, S=16),    # odd N = 25, prime D (wrapped edge tiles)
     dict(C=3, T=9, D=9, R=48, K=16, S=16),     # cov_tc at K = 16, SIMT apply (K % 64 != 0)
 ])
-@pytest.mark.parametrize("staged", [False, True])
-def test_edge_shapes(stap, kw, staged):
+@pytest.mark.parametrize("staged,prec", [(False, "fp32"), (True, "fp32"), (True, "tf32x3")])
+def test_edge_shapes(stap, kw, staged, prec):
     cfg = synth.StapConfig("edge", lam=1e-2, cfg_id=7, **kw)
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "random")
     ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
-    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    res = run_gpu(stap, cfg, cube, st, staged=staged, precision=prec)
     assert np.array_equal(res[2][0], ref["info"])
     assert rel_lines(res[1][0], ref["Y"]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("staged", [False, True])
-def test_info_paths(stap, staged):
-    cfg = synth.CONFIGS["small"]
+@pytest.mark.parametrize("name", ["small", "medium"])
+@pytest.mark.parametrize("staged,prec", [(False, "fp32"), (True, "fp32"), (True, "tf32x3")])
+def test_info_paths(stap, name, staged, prec):
+    cfg = synth.CONFIGS[name].with_(D=24) if name == "medium" else synth.CONFIGS[name]
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "random")
     cube[:, :, cfg.K:2 * cfg.K] = 0          # block 1 zero everywhere -> info = 1
     st[5] = 0                                 # steering 5 zero -> info = -6 elsewhere
     ref = oracle.run(OP(cfg), cube, st, nthreads=NT)
-    res = run_gpu(stap, cfg, cube, st, staged=staged)
+    res = run_gpu(stap, cfg, cube, st, staged=staged, precision=prec)
     Y, info = res[1][0], res[2][0]
     assert np.array_equal(info, ref["info"])
     assert np.all(info[:, 1] == 1) and np.all(info[:, 0] == -6)
@@ -427,8 +480,9 @@ def test_bad_pointer_alignment(stap):
 
 
 # ---------------------------------------------------------------- race / stability stress (compute-sanitizer is closed on this pool)
+@pytest.mark.parametrize("prec", ["fp32", "tf32x3"])
 @pytest.mark.parametrize("name", ["tiny", "small", "medium", "large"])
-def test_repeat_runs_bitwise(stap, name):
+def test_repeat_runs_bitwise(stap, name, prec):
     """Shared-memory races (mbarrier phases, aliased scratch, group barriers) show up as
     run-to-run differences: 8 repeated launches of every entry point must agree bitwise."""
     cfg = synth.CONFIGS[name]
@@ -436,7 +490,7 @@ def test_repeat_runs_bitwise(stap, name):
         cfg = cfg.with_(D=32)
     x = np.stack([synth.datacube(cfg, i) for i in range(2)])
     st = synth.steering(cfg, "random")
-    plan = plan_for(stap, cfg, batch=2)
+    plan = plan_for(stap, cfg, batch=2, precision=prec)
     dc, ds = dev(x).reshape(plan.cube_shape), dev(st)
     y0, i0 = plan.run(dc, ds)
     c0 = plan.covariance(dc)

@@ -1,6 +1,8 @@
 """Fused apply -> gather over NVLink peer stores (8(e) collective row).
 
-Two ranks, one GPU each: every rank's kernels store Y straight into rank 0's symmetric
+Two ranks, one GPU each.  --gather comm / comm-peer use the library's multi-GPU C ABI
+(stap_comm_*); the others hand torch symmetric-memory addresses to the same kernels: every
+rank's kernels store Y straight into rank 0's symmetric
 buffer (bench.py --gather peer); with peer-all every Y store is written locally and
 repeated into the peer's buffer (stap_params.out_n_peers); with multimem, every Y store is a multimem.st to the
 buffer's NVLS multicast address and lands in both ranks' buffers (--gather multimem).
@@ -20,13 +22,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gather", ["peer", "peer-all", "multimem"])
+@pytest.mark.parametrize("gather", ["comm", "comm-peer", "peer", "peer-all", "multimem"])
 @pytest.mark.parametrize("config", ["tiny", "small", "medium"])
 def test_peer_gather_bitwise_vs_nccl(config, gather):
+    """comm / comm-peer: the library's own stap_comm (C ABI: stap_comm_init_rank,
+    stap_comm_allgather_out, stap_comm_peer_offsets with CUDA IPC); peer / peer-all / multimem:
+    torch symmetric memory handing peer or multicast addresses to the same epilogue stores."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
+    port = 29611 + {"tiny": 0, "small": 1, "medium": 2}[config] + 5 * ["peer", "peer-all", "multimem", "comm",
+                                                                         "comm-peer"].index(gather)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str({"tiny": 29611, "small": 29612, "medium": 29613}[config] + {"peer": 0, "peer-all": 5, "multimem": 10}[gather]),
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--steps", "2", "--warmup", "3",
            "--gather", gather, "--no-stages", "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
