@@ -52,7 +52,9 @@ def test_comm_single_process_two_gpus(stap, name, prec):
         cubes.append(full.index_select(1, idx).contiguous().to(f"cuda:{r}"))
         plans.append(stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M, device=r,
                                    precision=prec))
-        outs.append(torch.full((G,) + plans[r].out_shape, float("nan"), dtype=torch.complex64, device=f"cuda:{r}"))
+        o = torch.empty((G,) + plans[r].out_shape, dtype=torch.complex64, device=f"cuda:{r}")
+        o.view(torch.float32).fill_(float("nan"))
+        outs.append(o)
         steers.append(st.to(f"cuda:{r}"))
     # expected gathered layout: [rank][batch][Dl][S][R]
     expect = torch.stack([ref[:, r * base.D:(r + 1) * base.D] for r in range(G)]).cpu()
@@ -70,7 +72,7 @@ def test_comm_single_process_two_gpus(stap, name, prec):
     offs = comm.peer_offsets(outs)
     assert all(len(o) == 1 for o in offs)
     for r in range(G):
-        outs[r].fill_(float("nan"))
+        outs[r].view(torch.float32).fill_(float("nan"))
     torch.cuda.synchronize(0)
     torch.cuda.synchronize(1)
     fplans = [stap.StapPlan(dims, dop_begin=p.dop_begin, dop_count=p.dop_count, cube_bin0=p.cube_bin0,

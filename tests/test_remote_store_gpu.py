@@ -58,7 +58,8 @@ def test_peer_copy_store_one_gpu(stap, name, D, path, prec, expect, entry):
     ds = torch.from_numpy(st).cuda(0)
     # one allocation holding both copies; the second at a 16-byte multiple past the first
     n = int(np.prod(plain.out_shape))
-    buf = torch.full((2 * n + 2,), float("nan"), dtype=torch.complex64, device="cuda:0")
+    buf = torch.empty((2 * n + 2,), dtype=torch.complex64, device="cuda:0")
+    buf.view(torch.float32).fill_(float("nan"))
     y0, y1 = buf[:n].view(plain.out_shape), buf[n + 2:2 * n + 2].view(plain.out_shape)
     off = y1.data_ptr() - y0.data_ptr()
     assert off % 16 == 0
