@@ -359,11 +359,13 @@ def main():
     ap.add_argument("--split", choices=["weak", "strong"], default="weak",
                     help="N > 1: weak = a D_cfg-bin slice per rank (configs[4]); strong = one D-bin cube split N ways")
     ap.add_argument("--gather", nargs="?", const="comm", default=None,
-                    choices=["comm", "comm-peer", "nccl", "nccl-root", "peer", "peer-all", "multimem"],
+                    choices=["comm", "comm-peer", "comm-push", "nccl", "nccl-root", "peer", "peer-all", "multimem"],
                     help="gather the outputs after each step: comm = the library's stap_comm_allgather_out "
                          "(in-place ncclAllGather; the default of a bare --gather); comm-peer = the library's "
                          "stap_comm_peer_offsets + out_n_peers: the all-gather fused into the apply epilogue by "
                          "peer stores (CUDA IPC mapping), a 1-float all-reduce per step as the device barrier; "
+                         "comm-push = the library's stap_comm_push_out: copy-engine peer copies of each step's "
+                         "slice on a second stream, overlapping the next step's covariance and solve; "
                          "baselines through torch: nccl = all_gather_into_tensor, nccl-root = gather to rank 0, "
                          "peer / peer-all / multimem = torch symmetric memory + the same epilogue stores "
                          "(SURVEY 8(f) NEXT-2)")
@@ -418,7 +420,7 @@ def main():
     gather_buf, y_dst, peer, offs, comm, step_bar = None, out, None, (), None, None
     if args.gather in ("peer", "peer-all", "multimem") and multi:
         gather_buf, y_dst, peer, offs = peer_gather_setup(out, world, rank, dev, dist, mode=args.gather)
-    elif args.gather in ("comm", "comm-peer") and multi:
+    elif args.gather in ("comm", "comm-peer", "comm-push") and multi:
         # the library's multi-GPU extension, one process per GPU: the NCCL unique id travels
         # over the torch process group, the communicator is libstap's own
         uid = [stap.StapComm.unique_id() if rank == 0 else None]
@@ -437,6 +439,8 @@ def main():
         if args.gather == "comm-peer":
             offs = comm.peer_offsets([gather_buf])[0]
             step_bar = torch.zeros(1, dtype=torch.float32, device=dev)
+        elif args.gather == "comm-push":
+            comm.peer_offsets([gather_buf])  # maps the peers' buffers; the plan's stores stay local
     pall = bool(offs) and multi
     plan = stap.StapPlan(dims, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
                          device=local_rank, path=args.path, out_multicast=mc, out_peer_offsets=offs,
@@ -464,6 +468,9 @@ def main():
         else:
             gather_buf = torch.empty((world,) + tuple(out.shape), dtype=torch.complex64, device=dev)
     s_ = stap._stream(stream, local_rank)
+    push = comm is not None and args.gather == "comm-push"
+    copy_stream = torch.cuda.Stream(dev) if push else None
+    copy_done = [None]  # the previous step's copy-engine gather (apply must not overwrite its source)
 
     ev_stage = []
 
@@ -478,13 +485,27 @@ def main():
             stap.stap_solve_weights(plan.handle, cov, steer, wts, gam, info, s_)
             if record:
                 e[2].record(stream)
+            if push and copy_done[0] is not None:
+                stream.wait_event(copy_done[0])
             stap.stap_apply(plan.handle, cube, wts, y_dst, s_)
             if record:
                 e[3].record(stream)
                 ev_stage.append(e)
         else:
+            if push and copy_done[0] is not None:
+                stream.wait_event(copy_done[0])
             stap.stap_run(plan.handle, cube, steer, y_dst, info, ws, plan.workspace_bytes, s_)
         if not multi or not args.gather:
+            return
+        if push:
+            # the gather of this step's slice by copy engines on the second stream, overlapping the
+            # next step's covariance and solve
+            done_apply = torch.cuda.Event()
+            done_apply.record(stream)
+            copy_stream.wait_event(done_apply)
+            comm.push_out([gather_buf], [plan], [copy_stream])
+            copy_done[0] = torch.cuda.Event()
+            copy_done[0].record(copy_stream)
             return
         if peer is not None:
             peer.barrier(channel=0)  # every rank's stores into the symmetric buffers have landed
@@ -517,6 +538,8 @@ def main():
             t0.record(stream)
             for _ in range(args.steps):
                 step(record=staged)
+            if copy_done[0] is not None:
+                stream.wait_event(copy_done[0])  # the last step's gather is inside the timed region
             t1.record(stream)
             barrier()
         el = t0.elapsed_time(t1) / 1e3
@@ -578,7 +601,7 @@ def main():
         pass
 
     gather_check = None
-    if multi and args.gather in ("peer", "peer-all", "multimem", "comm", "comm-peer"):
+    if multi and args.gather in ("peer", "peer-all", "multimem", "comm", "comm-peer", "comm-push"):
         # the gathered buffer must equal an NCCL all-gather of the local outputs, bitwise
         if staged:
             stap.stap_apply(plan_u.handle, cube, wts, out, s_)

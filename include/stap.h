@@ -227,6 +227,14 @@ stap_status stap_comm_allgather_out(stap_comm* comm, stap_c64* const* out_full, 
  * caller orders the stores before reading (stream sync + a barrier across ranks).  Collective:
  * every rank calls it with its own buffers.  n_peers = nranks - 1 <= 7. */
 stap_status stap_comm_peer_offsets(stap_comm* comm, stap_c64* const* out_full, int64_t* offsets, int32_t* n_peers);
+/* The gather by copy engines: for every local device i, enqueues on streams[i] one peer copy of
+ * this rank's slice of out_full[i] into every other rank's out_full (cudaMemcpyAsync over
+ * NVLink; no SM time, so it overlaps the next step's kernels when streams[i] is not the
+ * compute stream).  Needs a prior stap_comm_peer_offsets on the same out_full (the peer
+ * mapping), else STAP_ERR_BAD_DIMS; plans as in stap_comm_allgather_out.  The caller orders
+ * the copies before reading (stream sync + a barrier across ranks). */
+stap_status stap_comm_push_out(stap_comm* comm, stap_c64* const* out_full, const stap_plan* const* plans,
+                               const cudaStream_t* streams);
 /* Frees the NCCL communicators and closes the IPC mappings; NULL is accepted. */
 stap_status stap_comm_destroy(stap_comm* comm);
 

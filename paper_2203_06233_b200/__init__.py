@@ -34,7 +34,7 @@ SYMBOLS = ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes",
            "stap_doppler", "stap_covariance", "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host",
            "stap_status_string", "stap_abi_version",
            "stap_comm_unique_id", "stap_comm_create", "stap_comm_init_rank", "stap_comm_size",
-           "stap_comm_allgather_out", "stap_comm_peer_offsets", "stap_comm_destroy")
+           "stap_comm_allgather_out", "stap_comm_peer_offsets", "stap_comm_push_out", "stap_comm_destroy")
 
 
 class StapError(RuntimeError):
@@ -84,11 +84,12 @@ _lib.stap_comm_size.argtypes = [_vp, ctypes.POINTER(ctypes.c_int32), ctypes.POIN
 _lib.stap_comm_allgather_out.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
 _lib.stap_comm_peer_offsets.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64),
                                         ctypes.POINTER(ctypes.c_int32)]
+_lib.stap_comm_push_out.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
 _lib.stap_comm_destroy.argtypes = [_vp]
 for _f in ("stap_plan_create", "stap_plan_destroy", "stap_plan_workspace_bytes", "stap_doppler", "stap_covariance",
            "stap_solve_weights", "stap_apply", "stap_run", "stap_run_host", "stap_comm_unique_id",
            "stap_comm_create", "stap_comm_init_rank", "stap_comm_size", "stap_comm_allgather_out",
-           "stap_comm_peer_offsets", "stap_comm_destroy"):
+           "stap_comm_peer_offsets", "stap_comm_push_out", "stap_comm_destroy"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -385,6 +386,17 @@ class StapComm:
         pls = (_vp * n)(*[p.handle for p in plans])
         sts = (_vp * n)(*[s.cuda_stream for s in streams])
         _check(_lib.stap_comm_allgather_out(_vp(self.handle), bufs, pls, sts), "stap_comm_allgather_out")
+
+    def push_out(self, out_full, plans, streams=None):
+        """Copy-engine gather: this rank's slice of out_full[i] into every peer's out_full."""
+        import torch
+        n = self.nlocal
+        if streams is None:
+            streams = [torch.cuda.current_stream(d) for d in self.devices]
+        bufs = (_vp * n)(*[_ptr(t) for t in out_full])
+        pls = (_vp * n)(*[p.handle for p in plans])
+        sts = (_vp * n)(*[s.cuda_stream for s in streams])
+        _check(_lib.stap_comm_push_out(_vp(self.handle), bufs, pls, sts), "stap_comm_push_out")
 
     def peer_offsets(self, out_full):
         """Per local device, the byte offsets for stap_params.out_peer_offset (collective)."""

@@ -101,6 +101,10 @@ struct stap_comm {
   std::vector<ncclComm_t> comms;
   std::vector<void*> ipc_opened;  // peer allocations mapped by stap_comm_peer_offsets (closed at destroy)
   int ipc_device = -1;
+  // recorded by stap_comm_peer_offsets: per local device i, its out_full and every rank's
+  // out_full as addressable from this process (own rank: out_full[i] itself)
+  std::vector<char*> mapped_out;
+  std::vector<std::vector<char*>> peer_full;
 };
 
 extern "C" {
@@ -246,13 +250,18 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     if (reinterpret_cast<uintptr_t>(out_full[i]) & 15u) return STAP_ERR_MISALIGNED;
   }
   *n_peers = c->nranks - 1;
+  c->mapped_out.assign(c->nlocal, nullptr);
+  c->peer_full.assign(c->nlocal, std::vector<char*>(c->nranks, nullptr));
   if (c->nlocal == c->nranks) {
     // one process: every buffer is addressable from every device (peer access, unified VA)
     for (int i = 0; i < c->nlocal; ++i) {
+      c->mapped_out[i] = reinterpret_cast<char*>(out_full[i]);
       int k = 0;
-      for (int j = 0; j < c->nranks; ++j)
+      for (int j = 0; j < c->nranks; ++j) {
+        c->peer_full[i][j] = reinterpret_cast<char*>(out_full[j]);
         if (j != i)
           offsets[i * 7 + k++] = reinterpret_cast<char*>(out_full[j]) - reinterpret_cast<char*>(out_full[i]);
+      }
       for (; k < 7; ++k) offsets[i * 7 + k] = 0;
     }
     return STAP_OK;
@@ -295,6 +304,8 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     return STAP_ERR_NCCL;
   }
   int k = 0;
+  c->mapped_out[0] = reinterpret_cast<char*>(out_full[0]);
+  c->peer_full[0][c->ranks[0]] = reinterpret_cast<char*>(out_full[0]);
   for (int j = 0; j < c->nranks; ++j) {
     if (j == c->ranks[0]) continue;
     void* peer = nullptr;
@@ -304,9 +315,33 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     }
     c->ipc_opened.push_back(peer);
     c->ipc_device = c->devices[0];
-    offsets[k++] = (static_cast<char*>(peer) + all[j].offset) - reinterpret_cast<char*>(out_full[0]);
+    c->peer_full[0][j] = static_cast<char*>(peer) + all[j].offset;
+    offsets[k++] = c->peer_full[0][j] - reinterpret_cast<char*>(out_full[0]);
   }
   for (; k < 7; ++k) offsets[k] = 0;
+  return STAP_OK;
+}
+
+stap_status stap_comm_push_out(stap_comm* c, stap_c64* const* out_full, const stap_plan* const* plans,
+                               const cudaStream_t* streams) {
+  if (!c || !out_full || !plans || !streams) return STAP_ERR_NULL_ARG;
+  const size_t bytes = slice_bytes(c, plans);
+  if (!bytes) return STAP_ERR_BAD_DIMS;
+  if ((int)c->mapped_out.size() != c->nlocal) return STAP_ERR_BAD_DIMS;  // no stap_comm_peer_offsets yet
+  for (int i = 0; i < c->nlocal; ++i)
+    if (reinterpret_cast<char*>(out_full[i]) != c->mapped_out[i]) return STAP_ERR_BAD_DIMS;
+  for (int i = 0; i < c->nlocal; ++i) {
+    DevGuard g(c->devices[i]);
+    const size_t off = (size_t)c->ranks[i] * bytes;
+    for (int j = 0; j < c->nranks; ++j) {
+      if (j == c->ranks[i]) continue;
+      if (cudaMemcpyAsync(c->peer_full[i][j] + off, c->mapped_out[i] + off, bytes, cudaMemcpyDefault, streams[i]) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return STAP_ERR_CUDA;
+      }
+    }
+  }
   return STAP_OK;
 }
 

@@ -86,6 +86,20 @@ def test_comm_single_process_two_gpus(stap, name, prec):
     for r in range(G):
         assert torch.equal(outs[r].cpu().view(torch.float32), expect.view(torch.float32)), r
 
+    # (3) the gather by copy engines: plain local stores, then stap_comm_push_out
+    for r in range(G):
+        outs[r].view(torch.float32).fill_(float("nan"))
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    for r in range(G):
+        with torch.cuda.device(r):
+            plans[r].run(cubes[r], steers[r], out=outs[r][r])
+    comm.push_out(outs, plans)
+    for r in range(G):
+        torch.cuda.synchronize(r)
+    for r in range(G):
+        assert torch.equal(outs[r].cpu().view(torch.float32), expect.view(torch.float32)), r
+
 
 def test_comm_rejects_mismatched_plans(stap):
     if torch.cuda.device_count() < 2:

@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gather", ["comm", "comm-peer", "peer", "peer-all", "multimem"])
+@pytest.mark.parametrize("gather", ["comm", "comm-peer", "comm-push", "peer", "peer-all", "multimem"])
 @pytest.mark.parametrize("config", ["tiny", "small", "medium"])
 def test_peer_gather_bitwise_vs_nccl(config, gather):
     """comm / comm-peer: the library's own stap_comm (C ABI: stap_comm_init_rank,
@@ -31,7 +31,7 @@ def test_peer_gather_bitwise_vs_nccl(config, gather):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
     port = 29611 + {"tiny": 0, "small": 1, "medium": 2}[config] + 5 * ["peer", "peer-all", "multimem", "comm",
-                                                                         "comm-peer"].index(gather)
+                                                                         "comm-peer", "comm-push"].index(gather)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--steps", "2", "--warmup", "3",
