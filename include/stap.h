@@ -227,9 +227,10 @@ stap_status stap_comm_allgather_out(stap_comm* comm, stap_c64* const* out_full, 
  * caller orders the stores before reading (stream sync + a barrier across ranks).  Collective:
  * every rank calls it with its own buffers.  n_peers = nranks - 1 <= 7. */
 stap_status stap_comm_peer_offsets(stap_comm* comm, stap_c64* const* out_full, int64_t* offsets, int32_t* n_peers);
-/* The gather by copy engines: for every local device i, enqueues on streams[i] one peer copy of
- * this rank's slice of out_full[i] into every other rank's out_full (cudaMemcpyAsync over
- * NVLink; no SM time, so it overlaps the next step's kernels when streams[i] is not the
+/* The gather by copy engines: for every local device i, one peer copy of this rank's slice of
+ * out_full[i] into every other rank's out_full (cudaMemcpyAsync over NVLink, each peer's copy
+ * on its own internal stream -- its own copy engine -- forked from and joined back into
+ * streams[i]; no SM time, so it overlaps the next step's kernels when streams[i] is not the
  * compute stream).  Needs a prior stap_comm_peer_offsets on the same out_full (the peer
  * mapping), else STAP_ERR_BAD_DIMS; plans as in stap_comm_allgather_out.  The caller orders
  * the copies before reading (stream sync + a barrier across ranks). */

@@ -105,6 +105,11 @@ struct stap_comm {
   // out_full as addressable from this process (own rank: out_full[i] itself)
   std::vector<char*> mapped_out;
   std::vector<std::vector<char*>> peer_full;
+  // stap_comm_push_out's fork-join: per local device, one stream per peer (the copies to
+  // different peers run on different copy engines) and the events that chain them
+  std::vector<std::vector<cudaStream_t>> push_streams;
+  std::vector<cudaEvent_t> push_fork;
+  std::vector<std::vector<cudaEvent_t>> push_join;
 };
 
 extern "C" {
@@ -330,16 +335,42 @@ stap_status stap_comm_push_out(stap_comm* c, stap_c64* const* out_full, const st
   if ((int)c->mapped_out.size() != c->nlocal) return STAP_ERR_BAD_DIMS;  // no stap_comm_peer_offsets yet
   for (int i = 0; i < c->nlocal; ++i)
     if (reinterpret_cast<char*>(out_full[i]) != c->mapped_out[i]) return STAP_ERR_BAD_DIMS;
-  for (int i = 0; i < c->nlocal; ++i) {
-    DevGuard g(c->devices[i]);
-    const size_t off = (size_t)c->ranks[i] * bytes;
-    for (int j = 0; j < c->nranks; ++j) {
-      if (j == c->ranks[i]) continue;
-      if (cudaMemcpyAsync(c->peer_full[i][j] + off, c->mapped_out[i] + off, bytes, cudaMemcpyDefault, streams[i]) !=
-          cudaSuccess) {
+  if (c->push_streams.empty()) {  // created once per communicator
+    c->push_streams.assign(c->nlocal, std::vector<cudaStream_t>(c->nranks, nullptr));
+    c->push_join.assign(c->nlocal, std::vector<cudaEvent_t>(c->nranks, nullptr));
+    c->push_fork.assign(c->nlocal, nullptr);
+    for (int i = 0; i < c->nlocal; ++i) {
+      DevGuard g(c->devices[i]);
+      bool ok = cudaEventCreateWithFlags(&c->push_fork[i], cudaEventDisableTiming) == cudaSuccess;
+      for (int j = 0; j < c->nranks && ok; ++j) {
+        if (j == c->ranks[i]) continue;
+        ok = cudaStreamCreateWithFlags(&c->push_streams[i][j], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->push_join[i][j], cudaEventDisableTiming) == cudaSuccess;
+      }
+      if (!ok) {
         cudaGetLastError();
         return STAP_ERR_CUDA;
       }
+    }
+  }
+  // fork: every peer copy waits for the caller's stream, runs on its own stream (its own copy
+  // engine), and the caller's stream waits for all of them (join)
+  for (int i = 0; i < c->nlocal; ++i) {
+    DevGuard g(c->devices[i]);
+    const size_t off = (size_t)c->ranks[i] * bytes;
+    bool ok = cudaEventRecord(c->push_fork[i], streams[i]) == cudaSuccess;
+    for (int j = 0; j < c->nranks && ok; ++j) {
+      if (j == c->ranks[i]) continue;
+      cudaStream_t q = c->push_streams[i][j];
+      ok = cudaStreamWaitEvent(q, c->push_fork[i], 0) == cudaSuccess &&
+           cudaMemcpyAsync(c->peer_full[i][j] + off, c->mapped_out[i] + off, bytes, cudaMemcpyDefault, q) ==
+               cudaSuccess &&
+           cudaEventRecord(c->push_join[i][j], q) == cudaSuccess &&
+           cudaStreamWaitEvent(streams[i], c->push_join[i][j], 0) == cudaSuccess;
+    }
+    if (!ok) {
+      cudaGetLastError();
+      return STAP_ERR_CUDA;
     }
   }
   return STAP_OK;
@@ -347,6 +378,14 @@ stap_status stap_comm_push_out(stap_comm* c, stap_c64* const* out_full, const st
 
 stap_status stap_comm_destroy(stap_comm* c) {
   if (!c) return STAP_OK;
+  for (size_t i = 0; i < c->push_streams.size(); ++i) {
+    DevGuard g(c->devices[i]);
+    for (cudaStream_t q : c->push_streams[i])
+      if (q) cudaStreamDestroy(q);
+    for (cudaEvent_t e : c->push_join[i])
+      if (e) cudaEventDestroy(e);
+    if (c->push_fork[i]) cudaEventDestroy(c->push_fork[i]);
+  }
   if (!c->ipc_opened.empty()) {
     DevGuard g(c->ipc_device);
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);

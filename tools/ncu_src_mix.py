@@ -1,7 +1,8 @@
 """Aggregate ncu source-page (SASS) stall samples by opcode: python tools/ncu_src_mix.py src.csv"""
 import csv, sys, collections
 rows = list(csv.reader(open(sys.argv[1])))
-h = rows[1]; data = rows[2:]
+off = 0 if "Source" in rows[0] else 1
+h = rows[off]; data = rows[off + 1:]
 iS = h.index("Source"); ie = h.index("Instructions Executed")
 cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 agg = collections.defaultdict(lambda: collections.Counter())
