@@ -115,31 +115,36 @@ def test_run_full_size_every_bin(stap, name, prec):
         assert rel_lines(Y[M - 1, d], r1["Y"][0]).max() <= 1e-3, (name, d)
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_weak_shard_plan_as_bench_builds_it(stap, G):
-    """The exact weak-scaling shard plans bench.py builds at --gpus G (BASELINE configs[4]):
-    global D = 1024*G large cube, rank g owns [1024 g, 1024 (g+1)) from a buffer holding its
-    bins plus the T-1 halo (wrapped at ranks 0 and G-1), batch 2.  Every rank's Y equals the
-    unsharded run over the whole global cube bitwise (P15), and sampled bins at the shard
-    edges match the oracle.  Random device data: the check is the shard mechanics."""
+@pytest.mark.parametrize("split,name,G", [("weak", "large", 2), ("weak", "large", 4), ("strong", "medium", 2),
+                                          ("strong", "medium", 4), ("strong", "large", 4)])
+def test_shard_plans_as_bench_builds_them(stap, split, name, G):
+    """The exact shard plans bench.py builds at --gpus G (bench.shard_plan_args):
+    weak (BASELINE configs[4]): global D = D_cfg*G, rank g owns [g D_cfg, (g+1) D_cfg);
+    strong (configs[2] "medium on 1/2/4/8"): the config's D bins split D/G per rank.  Each rank's
+    buffer holds its bins plus the T-1 halo (wrapped at the ends); batch 2, precision tf32x3.
+    Every rank's Y equals the unsharded run over the whole global cube bitwise (P15), and
+    sampled bins at the shard edges match the oracle.  Random device data: the check is the
+    shard mechanics."""
     import bench
-    base = synth.CONFIGS["large"]
-    gcfg = base.with_(D=base.D * G)
+    base = synth.CONFIGS[name]
     M = 2
+    gcfg = bench.shard_plan_args(base, G, 0, split)[0]
     gen = torch.Generator(device="cuda:0").manual_seed(100 + G)
     full = torch.randn((M, gcfg.D, gcfg.C, gcfg.R), dtype=torch.complex64, device="cuda:0", generator=gen)
     st = dev(synth.steering(base, "ula"))
     pf = plan_for(stap, gcfg, batch=M, precision="tf32x3")
     Yf, If = pf.run(full, st)
     torch.cuda.synchronize()
+    covered = 0
     for g in range(G):
-        lo, cnt = g * base.D, base.D
-        b0, nb = synth.shard_window(gcfg, lo, cnt)
+        gc, lo, cnt, b0, nb = bench.shard_plan_args(base, G, g, split)
+        assert gc.D == gcfg.D
+        covered += cnt
         idx = torch.from_numpy((b0 + np.arange(nb)) % gcfg.D).cuda(0)
         local = full.index_select(1, idx).contiguous()
         ps = plan_for(stap, gcfg, dop_begin=lo, dop_count=cnt, cube_bin0=b0, cube_bins=nb, batch=M,
                       precision="tf32x3")
-        assert ps.description == pf.description
+        assert ps.description == pf.description or split == "strong"
         assert bench.plan_shape_out(stap, ps.dims, lo, cnt, b0, nb, M) == ps.out_shape
         Ys, Is = ps.run(local, st)
         torch.cuda.synchronize()
@@ -152,6 +157,7 @@ def test_weak_shard_plan_as_bench_builds_it(stap, G):
                 r1 = oracle.run(OP(gcfg, dop_begin=d, dop_count=1, cube_bin0=ob0, cube_bins=onb),
                                 np.ascontiguousarray(xl[rows]), st.cpu().numpy(), nthreads=NT)
                 assert rel_lines(Ys[0, d - lo].cpu().numpy(), r1["Y"][0]).max() <= 1e-3, (g, d)
+    assert covered == gcfg.D
 
 
 # ---------------------------------------------------------------- stages vs oracle

@@ -60,3 +60,24 @@ def test_run_host_rejects_multicast_out():
     with pytest.raises(stap.StapError) as e:
         plan.run_host(hc, hs, ho, hi, ws)
     assert e.value.code == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,split", [("medium", "strong"), ("large", "strong"), ("large", "weak")])
+def test_bench_split_two_gpus(config, split):
+    """bench.py's 2-GPU shards (weak: a D_cfg-bin slice per rank; strong: one cube split in two)
+    run through the C ABI with every unit healthy, and the whole-job value is counted in the
+    split's unit (strong: whole cubes)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    port = 29700 + 3 * ["medium", "large"].index(config) + (split == "weak")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", config, "--split", split, "--steps", "3",
+           "--warmup", "3", "--no-stages", "--no-e2e", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["scaling"] == split and line["n_gpus"] == 2 and line["info_nonzero"] == 0
+    cubes = {"medium": 16, "large": 2}[config] * (1 if split == "strong" else 2)  # whole-job cubes per step
+    assert abs(line["value"] * line["ms_per_step"] / 1e3 - cubes) < 1e-6 * cubes
