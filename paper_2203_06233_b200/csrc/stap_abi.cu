@@ -380,6 +380,16 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
   int major = 0;
   if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device) != cudaSuccess || major != 10)
     return STAP_ERR_DEVICE;
+  {
+    // the tensor-map encoder (a driver call, used below to decide the tcgen05 stages) needs the
+    // device's primary context: create it here, so that a plan made before any other CUDA call
+    // in the process selects exactly the kernels any later plan of the same parameters does
+    DeviceGuard g(p->device);
+    if (!g.ok || cudaFree(nullptr) != cudaSuccess) {
+      cudaGetLastError();
+      return STAP_ERR_DEVICE;
+    }
+  }
 
   stap_plan* pl = new (std::nothrow) stap_plan();
   if (!pl) return STAP_ERR_CUDA;

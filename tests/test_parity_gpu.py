@@ -320,6 +320,22 @@ def test_path_and_precision_selection(stap):
     assert plan_for(stap, synth.CONFIGS["small"], precision="tf32x3").description.startswith("fused")
 
 
+def test_plan_as_first_cuda_call(stap):
+    """A plan created before any other CUDA call in a fresh process selects the same kernels as
+    any later plan (the tcgen05 stages depend on a driver tensor-map encode, which needs the
+    primary context: stap_plan_create creates it).  Round 2 found a first plan silently on the
+    SIMT covariance and apply."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import synth, paper_2203_06233_b200 as p\n"
+            "c = synth.CONFIGS['large']\n"
+            "print(p.StapPlan(p.Dims(c.C, c.T, c.D, c.R, c.K, c.S, c.lam), precision='tf32x3').description)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
+                         check=True).stdout
+    assert "cov(tcgen05" in out and "apply(tcgen05" in out, out
+
+
 # ---------------------------------------------------------------- composition, shards, batch, determinism
 @pytest.mark.parametrize("name", ["small", "medium"])
 def test_fused_equals_staged(stap, name):
