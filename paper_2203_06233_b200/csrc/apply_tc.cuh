@@ -3,8 +3,9 @@
 // when S = 16, K % 64 == 0 and N <= 64 (medium / large); the SIMT apply (apply.cuh)
 // covers every other shape.
 //
-// Method: Y[d][k][r] = w_{d,b(r),k}^H z_{d,r} (reading c-12; PAPER.md "Beamforming"
-// / Fig. 1 "apply weights"), written as one real GEMM per tile of 64 range cells of
+// Method (include/stap.h; reading c-12 -- the paper shows the STAP kernel only as
+// a figure, whose statement U is the 2-D x 2-D array multiply of
+// PAPER.md:420-425): Y[d][k][r] = w_{d,b(r),k}^H z_{d,r}, written as one real GEMM per tile of 64 range cells of
 // a unit (d, b):
 //   rows    m = 2*jj + part, jj < 64 the cell, part 0 = Re z, 1 = Im z   -> M = 128
 //   columns n < S: Re w_k,  n >= S: Im w_{n-S}                          -> N = 2S = 32

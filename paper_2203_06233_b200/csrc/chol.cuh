@@ -600,10 +600,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // ---- host-side selection ---------------------------------------------------
 // Instantiations (N > 16; N <= 16 runs solve_small.cuh).  Measured on B200 (65536 large /
 // 131072 medium matrices, S = 16): 4x8 lanes, 14x7 blocks, 128 threads x 2 blocks/SM: 1.60 ms
-// (old 8x8 two-warp group solver 2.23 ms); N <= 32: 4x8 lanes, 8x4 blocks: 1.04 ms (old 1.22).
+// (old 8x8 two-warp group solver 2.23 ms); N <= 32: 4x8 lanes, 8x4 blocks, 256 threads x 2
+// blocks/SM (128 registers): 0.997 ms (128 x 3 at 136 registers: 1.036 ms; old 1.22).
 #define STAPK_CHOL_CFGS(X)                                      \
   X(0, (CholCfg<4, 8, 8, 4, 1, false, 2>), 128, 3)              \
-  X(1, (CholCfg<4, 8, 8, 4, 2, false, 2>), 128, 3)              \
+  X(1, (CholCfg<4, 8, 8, 4, 2, false, 2>), 256, 2)              \
   X(2, (CholCfg<4, 8, 8, 4, 4, false, 2>), 128, 2)              \
   X(3, (CholCfg<4, 8, 14, 7, 1, false, 2>), 128, 2)             \
   X(4, (CholCfg<4, 8, 14, 7, 2, false, 2>), 128, 2)             \

@@ -1,6 +1,7 @@
 // cov_tc.cuh -- K1 on the 5th-generation tensor cores (tcgen05.mma kind::tf32, 3xTF32).
 //
-// Method (reading c-4..c-7; PAPER.md "covariance estimation"): R_hat_d =
+// Method (include/stap.h; readings c-4..c-7 -- the paper gives the STAP kernel
+// only as a figure): R_hat_d =
 // (1/K) sum_r z_r z_r^H over the K cells of a training block, z_r[t*C + c] =
 // X[d-h+t][c][r]; R_d = R_hat_d + delta_d I, delta_d = lambda tr(R_hat_d) / N.
 //
