@@ -90,15 +90,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// try_wait with a suspend-time hint (ns): a waiting thread sleeps in hardware until the phase
+// completes (or the hint expires) instead of re-issuing the test, so waiting warps stop taking
+// issue slots (measured: cov_tc 566 -> 564 us, medium 450 -> 445 us)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(10000000u)
       : "memory");
 }
 
