@@ -322,7 +322,7 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_obj(args, cfg, world):
+def config_obj(args, cfg, world, path=None):
     if world > 1 and args.split == "strong":
         par = f"doppler-shard x{world} (strong: D = {cfg.D} split {cfg.D // world} bins per rank + halo)"
         per_gpu = f"{args.cubes} cubes x 1/{world} of the bins"
@@ -331,9 +331,17 @@ def config_obj(args, cfg, world):
         per_gpu = args.cubes
     return {"workload": WORKLOAD_DESC.get(cfg.name, cfg.name), "C": cfg.C, "TDOF": cfg.T, "D": cfg.D, "R": cfg.R,
             "S": cfg.S, "K": cfg.K, "lambda": cfg.lam, "cubes_per_step_per_gpu": per_gpu,
-            "parallelism": par, "precision": PRECISION_DESC[args.precision],
+            "parallelism": par, "precision": precision_desc(args.precision, path),
             "l2": "inputs larger than L2 (no flush)", "steering": "ULA centre-bin",
             **({"gather": args.gather} if args.gather and world > 1 else {})}
+
+
+def precision_desc(prec, path):
+    """The arithmetic the timed path actually runs (the plan decides per shape)."""
+    if prec == "tf32x3" and path is not None and "tcgen05" not in path:
+        return ("stap_params.precision=STAP_PREC_TF32X3 requested; this shape's path (" + path.split(":")[0] +
+                ") has no tcgen05 stage, so every stage runs FP32 FFMA")
+    return PRECISION_DESC[prec]
 
 
 PRECISION_DESC = {
@@ -621,7 +629,7 @@ def main():
         "metric": "STAP datacubes/sec", "value": value, "unit": "cubes/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_obj(args, cfg, world),
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_obj(args, cfg, world, plan.description),
         "path": plan.description, "gpu_launches": launches_per_step * args.steps, "roofline": roof,
         "clocks": clocks, "info_nonzero": ninfo_bad,
     }
