@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
   uint64_t* a_full = empty + ns;   // A (TMEM) and B (smem) of the tile written
   uint64_t* mma_bar = a_full + 1;  // the tile's MMAs done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // warp index and TMEM base broadcast from lane 0: provably warp-uniform, so the compiler keeps
+  // them (and the TMEM addresses derived from them) in uniform registers
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kApplyTcThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int MT = K / 64;
   const int G = gridDim.x;
   const int my_units = (int)blockIdx.x < units ? (units - (int)blockIdx.x + G - 1) / G : 0;
