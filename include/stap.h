@@ -225,7 +225,9 @@ stap_status stap_comm_allgather_out(stap_comm* comm, stap_c64* const* out_full, 
  * cudaMalloc allocation or lie inside one).  Passing them as stap_params.out_n_peers /
  * out_peer_offset makes every Y store of stap_run / stap_apply land in every rank's buffer; the
  * caller orders the stores before reading (stream sync + a barrier across ranks).  Collective:
- * every rank calls it with its own buffers.  n_peers = nranks - 1 <= 7. */
+ * every rank calls it with its own buffers; a repeat call with the buffers of the previous call
+ * returns the same offsets without communicating (peers stay mapped until stap_comm_destroy).
+ * n_peers = nranks - 1 <= 7. */
 stap_status stap_comm_peer_offsets(stap_comm* comm, stap_c64* const* out_full, int64_t* offsets, int32_t* n_peers);
 /* The gather by copy engines: for every local device i, one peer copy of this rank's slice of
  * out_full[i] into every other rank's out_full (cudaMemcpyAsync over NVLink, each peer's copy

@@ -255,12 +255,23 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     if (reinterpret_cast<uintptr_t>(out_full[i]) & 15u) return STAP_ERR_MISALIGNED;
   }
   *n_peers = c->nranks - 1;
-  c->mapped_out.assign(c->nlocal, nullptr);
+  // the same buffers again: the peers are mapped already (an IPC handle opens once per process)
+  bool same = (int)c->mapped_out.size() == c->nlocal;
+  for (int i = 0; i < c->nlocal && same; ++i) same = c->mapped_out[i] == reinterpret_cast<char*>(out_full[i]);
+  if (same) {
+    for (int i = 0; i < c->nlocal; ++i) {
+      int k = 0;
+      for (int j = 0; j < c->nranks; ++j)
+        if (j != c->ranks[i]) offsets[i * 7 + k++] = c->peer_full[i][j] - c->mapped_out[i];
+      for (; k < 7; ++k) offsets[i * 7 + k] = 0;
+    }
+    return STAP_OK;
+  }
+  c->mapped_out.clear();  // set again only once every peer is mapped (stap_comm_push_out checks it)
   c->peer_full.assign(c->nlocal, std::vector<char*>(c->nranks, nullptr));
   if (c->nlocal == c->nranks) {
     // one process: every buffer is addressable from every device (peer access, unified VA)
     for (int i = 0; i < c->nlocal; ++i) {
-      c->mapped_out[i] = reinterpret_cast<char*>(out_full[i]);
       int k = 0;
       for (int j = 0; j < c->nranks; ++j) {
         c->peer_full[i][j] = reinterpret_cast<char*>(out_full[j]);
@@ -269,6 +280,7 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
       }
       for (; k < 7; ++k) offsets[i * 7 + k] = 0;
     }
+    c->mapped_out.assign(reinterpret_cast<char* const*>(out_full), reinterpret_cast<char* const*>(out_full) + c->nlocal);
     return STAP_OK;
   }
   // one process per GPU: publish (IPC handle of the allocation, offset) through the
@@ -309,7 +321,6 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     return STAP_ERR_NCCL;
   }
   int k = 0;
-  c->mapped_out[0] = reinterpret_cast<char*>(out_full[0]);
   c->peer_full[0][c->ranks[0]] = reinterpret_cast<char*>(out_full[0]);
   for (int j = 0; j < c->nranks; ++j) {
     if (j == c->ranks[0]) continue;
@@ -324,6 +335,7 @@ stap_status stap_comm_peer_offsets(stap_comm* c, stap_c64* const* out_full, int6
     offsets[k++] = c->peer_full[0][j] - reinterpret_cast<char*>(out_full[0]);
   }
   for (; k < 7; ++k) offsets[k] = 0;
+  c->mapped_out.assign(1, reinterpret_cast<char*>(out_full[0]));
   return STAP_OK;
 }
 

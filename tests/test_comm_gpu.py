@@ -71,6 +71,7 @@ def test_comm_single_process_two_gpus(stap, name, prec):
     # (2) the all-gather fused into the apply epilogue: peer-copy stores, no collective call
     offs = comm.peer_offsets(outs)
     assert all(len(o) == 1 for o in offs)
+    assert comm.peer_offsets(outs) == offs  # a repeat call with the same buffers: the same offsets
     for r in range(G):
         outs[r].view(torch.float32).fill_(float("nan"))
     torch.cuda.synchronize(0)
@@ -99,6 +100,11 @@ def test_comm_single_process_two_gpus(stap, name, prec):
         torch.cuda.synchronize(r)
     for r in range(G):
         assert torch.equal(outs[r].cpu().view(torch.float32), expect.view(torch.float32)), r
+    # push_out needs the buffers peer_offsets mapped
+    other = [torch.empty_like(o) for o in outs]
+    with pytest.raises(stap.StapError) as e:
+        comm.push_out(other, plans)
+    assert e.value.code == 2
 
 
 def test_comm_rejects_mismatched_plans(stap):
