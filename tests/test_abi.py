@@ -109,3 +109,30 @@ def test_no_device_no_fallback(pkg):
         pytest.skip("a GPU is present")
     h = ctypes.c_void_p()
     assert pkg._lib.stap_plan_create(ctypes.byref(_params(pkg)), ctypes.byref(h)) == 7
+
+
+def test_header_is_plain_c(tmp_path, pkg):
+    """include/stap.h compiles as C11 and a C program links libstap.so through it (the C ABI
+    is consumable without Python); only device-free entry points are called here."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "use_stap.c"
+    src.write_text(
+        '#include "stap.h"\n#include <stdio.h>\n#include <string.h>\n'
+        "int main(void) {\n"
+        "  stap_plan* p = 0;\n"
+        "  if (stap_plan_create(0, &p) != STAP_ERR_NULL_ARG) return 1;\n"
+        "  if (strncmp(stap_status_string(STAP_ERR_NCCL), \"STAP_ERR_NCCL\", 13) != 0) return 2;\n"
+        "  printf(\"%d\\n\", stap_abi_version());\n"
+        "  return 0;\n}\n")
+    exe = tmp_path / "use_stap"
+    libdir = os.path.join(root, "paper_2203_06233_b200")
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Werror", "-I", os.path.join(root, "include"), "-I",
+                    "/usr/local/cuda/include", str(src), "-L", libdir, "-lstap", f"-Wl,-rpath,{libdir}",
+                    "-o", str(exe)], check=True, capture_output=True, text=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    assert int(out) == pkg.stap_abi_version()
