@@ -599,15 +599,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 
 // ---- host-side selection ---------------------------------------------------
 // Instantiations (N > 16; N <= 16 runs solve_small.cuh).  Measured on B200 (65536 large /
-// 131072 medium matrices, S = 16): 4x8 lanes, 14x7 blocks, 128 threads x 2 blocks/SM: 1.60 ms
-// (old 8x8 two-warp group solver 2.23 ms); N <= 32: 4x8 lanes, 8x4 blocks, 256 threads x 2
-// blocks/SM (128 registers): 0.997 ms (128 x 3 at 136 registers: 1.036 ms; old 1.22).
+// 131072 medium matrices, S = 16): 4x8 lanes, 14x7 blocks, one 256-thread block per SM (8
+// warps): 1.583 ms (2 x 128: 1.611 ms; 4 x 64: 1.684 ms; old 8x8 two-warp group solver 2.23 ms);
+// N <= 32: 4x8 lanes, 8x4 blocks, one 512-thread block per SM (16 warps, 128 registers):
+// 0.943 ms (2 x 256: 0.998 ms; 3 x 128 at 136 registers: 1.036 ms; 8 x 64: 1.055 ms; old
+// 1.22).  Same warps per SM, one block: the results are bitwise those of the smaller blocks.
 #define STAPK_CHOL_CFGS(X)                                      \
   X(0, (CholCfg<4, 8, 8, 4, 1, false, 2>), 128, 3)              \
-  X(1, (CholCfg<4, 8, 8, 4, 2, false, 2>), 256, 2)              \
+  X(1, (CholCfg<4, 8, 8, 4, 2, false, 2>), 512, 1)              \
   X(2, (CholCfg<4, 8, 8, 4, 4, false, 2>), 128, 2)              \
-  X(3, (CholCfg<4, 8, 14, 7, 1, false, 2>), 128, 2)             \
-  X(4, (CholCfg<4, 8, 14, 7, 2, false, 2>), 128, 2)             \
+  X(3, (CholCfg<4, 8, 14, 7, 1, false, 2>), 256, 1)             \
+  X(4, (CholCfg<4, 8, 14, 7, 2, false, 2>), 256, 1)             \
   X(5, (CholCfg<8, 8, 7, 7, 4, false, 4>), 64, 4)               \
   X(6, (CholCfg<8, 8, 8, 8, 1, false, 4>), 64, 5)               \
   X(7, (CholCfg<8, 8, 8, 8, 2, false, 4>), 64, 5)               \
