@@ -477,10 +477,11 @@ def test_edge_shapes(stap, kw, staged, prec):
     assert rel_lines(res[1][0], ref["Y"]).max() <= 1e-3
 
 
-@pytest.mark.parametrize("name", ["small", "medium"])
+@pytest.mark.parametrize("name", ["small", "medium", "large"])
 @pytest.mark.parametrize("staged,prec", [(False, "fp32"), (True, "fp32"), (True, "tf32x3")])
 def test_info_paths(stap, name, staged, prec):
-    cfg = synth.CONFIGS[name].with_(D=24) if name == "medium" else synth.CONFIGS[name]
+    cfg = {"medium": synth.CONFIGS["medium"].with_(D=24),
+           "large": synth.CONFIGS["large"].with_(D=16, R=512)}.get(name, synth.CONFIGS[name])
     cube = synth.datacube(cfg)
     st = synth.steering(cfg, "random")
     cube[:, :, cfg.K:2 * cfg.K] = 0          # block 1 zero everywhere -> info = 1
