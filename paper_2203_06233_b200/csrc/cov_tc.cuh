@@ -19,8 +19,8 @@
 //
 // Data movement: a producer warp TMA-loads each chunk of the tile (one box {32
 // floats, MB*C rows} of the cube viewed as [batch*nbins*C rows][2R floats], 128-byte
-// swizzled so that a thread reading its own row is bank-conflict free) into a 4-stage
-// ring; the rare tiles whose bins wrap around the cube's edge read rows from global.
+// swizzled so that a thread reading its own row is bank-conflict free) into a ring of
+// 2-4 stages (as many as the shared memory holds: 3 at large, 4 at medium); the rare tiles whose bins wrap around the cube's edge read rows from global.
 // Four compute warps (thread m = Gram row m = TMEM lane m) read their row, split it
 // and write (a) the A operand into their TMEM lane (the "TS" form: A never touches
 // shared memory again) and (b) the B operand planes (Re hi, Im hi, Re lo, Im lo,
@@ -49,10 +49,6 @@ __device__ unsigned long long g_covtc_prof[8];  // [6] = tiles; [7] = band copy 
 constexpr int kCovTcCompute = 4;  // compute warps: TMEM lanes 0..127
 constexpr int kCovTcWriter = 8;   // writer warps: R_d assembly and stores, overlapped with the next tile
 constexpr int kCovTcThreads = (kCovTcCompute + kCovTcWriter) * 32 + 64;  // + producer warp + MMA warp
-#ifndef COVTC_STAGES
-#define COVTC_STAGES 2
-#endif
-constexpr int kCovTcStages = COVTC_STAGES;
 constexpr uint32_t kCovTcRawBytes = 128u * 128u;        // a chunk: 128 rows x 32 floats (16 cells)
 constexpr uint32_t kCovTcPlaneBytes = 128u * 16u * 4u;  // a B plane: 128 rows x 16 cells
 constexpr uint32_t kCovTcBBytes = 4u * kCovTcPlaneBytes;  // Re hi | Im hi | Re lo | Im lo
@@ -63,6 +59,7 @@ struct CovTcGeom {
   int OB;   // output bins per tile = MB - T + 1
   int ntd;  // tiles along the owned Doppler range
   int RS;   // row stride (float2) of the Gram band buffer: >= N with RS - 1 odd (conflict-free)
+  int NS;   // stages of the TMA chunk ring: as many (2..4) as fit the shared memory
 };
 __host__ inline CovTcGeom cov_tc_geom(int C, int T, int N, int dop_count) {
   CovTcGeom g;
@@ -70,6 +67,7 @@ __host__ inline CovTcGeom cov_tc_geom(int C, int T, int N, int dop_count) {
   g.OB = g.MB - T + 1;
   g.ntd = g.OB > 0 ? (dop_count + g.OB - 1) / g.OB : 0;
   g.RS = (N & 1) ? N + 1 : N;  // RS - 1 odd: band writes and mirrored reads of consecutive lanes
+  g.NS = 2;                     // set by the plan (cov_tc_smem decides what fits)
   return g;
 }
 // Where it is used: the 128 x 128 Gram tile is worth it only when the window (N = T*C
@@ -81,14 +79,14 @@ __host__ inline bool cov_tc_supported(int C, int T, int N, int K) {
 struct CovTcSmem {
   size_t raw, bpl, rbuf, delta, bar, total;
 };
-__host__ __device__ inline CovTcSmem cov_tc_smem(int N, int RS, int OB) {
+__host__ __device__ inline CovTcSmem cov_tc_smem(int N, int RS, int OB, int NS) {
   CovTcSmem s;
   s.raw = 0;                                           // stages (1024-aligned for the swizzle)
-  s.bpl = s.raw + (size_t)kCovTcStages * kCovTcRawBytes;  // B planes x 2
+  s.bpl = s.raw + (size_t)NS * kCovTcRawBytes;         // B planes x 2
   s.rbuf = s.bpl + 2 * (size_t)kCovTcBBytes;           // Gram band x 2 [128][RS]
   s.delta = s.rbuf + 2 * (size_t)128 * RS * 8;         // delta x 2 [OB]
   s.bar = s.delta + 2 * (((size_t)OB * 4 + 15) & ~(size_t)15);
-  s.total = s.bar + (2 * kCovTcStages + 8) * 8 + 16 + 1024;  // + alignment slack
+  s.total = s.bar + (2 * NS + 8) * 8 + 16 + 1024;  // + alignment slack
   return s;
 }
 
@@ -98,15 +96,16 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int C = p.C, T = p.T, N = p.N, K = p.K;
-  const CovTcSmem L = cov_tc_smem(N, g.RS, g.OB);
+  const CovTcSmem L = cov_tc_smem(N, g.RS, g.OB, g.NS);
+  const int NS = g.NS;
   unsigned char* raw = smem + L.raw;
   unsigned char* bpl = smem + L.bpl;
   float2* gband0 = reinterpret_cast<float2*>(smem + L.rbuf);  // [2][128][RS]: band G[m][m+k] / K
   float* delta0 = reinterpret_cast<float*>(smem + L.delta);    // [2][OB4]
   const int OB4 = ((g.OB + 3) & ~3);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);  // [stages]
-  uint64_t* empty = full + kCovTcStages;                        // [stages]
-  uint64_t* a_full = empty + kCovTcStages;                      // [2] by chunk parity
+  uint64_t* empty = full + NS;                        // [stages]
+  uint64_t* a_full = empty + NS;                      // [2] by chunk parity
   uint64_t* mma_done = a_full + 2;                              // [2] by chunk parity
   uint64_t* gb_full = mma_done + 2;   // [2] by tile parity: band written (compute -> writers)
   uint64_t* gb_empty = gb_full + 2;   // [2] by tile parity: band consumed (writers -> compute)
@@ -121,7 +120,7 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < kCovTcStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCompute);
     }
@@ -134,7 +133,7 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
     fence_mbar_init();
   }
   // rows a tile leaves unloaded (MB*C < 128) must hold finite values
-  for (uint32_t i = tid; i < kCovTcStages * kCovTcRawBytes / 16; i += blockDim.x)
+  for (uint32_t i = tid; i < NS * kCovTcRawBytes / 16; i += blockDim.x)
     reinterpret_cast<float4*>(raw)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   fence_proxy_async();
   tc_fence_before();
@@ -219,7 +218,7 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
         const Tile t = decode(tt);
         const int y0 = t.n * p.nbins * C;
         for (int ch = 0; ch < nch; ++ch, ++cc) {
-          if (cc >= kCovTcStages) mbar_wait(&empty[s], ph ^ 1u);
+          if (cc >= NS) mbar_wait(&empty[s], ph ^ 1u);
           unsigned char* dst = raw + (size_t)s * kCovTcRawBytes;
           const int x = 2 * (t.b * K + 16 * ch);
           if (!t.wrap) {
@@ -228,7 +227,7 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
           } else {
             mbar_arrive(&full[s]);  // wrapped tile: the compute warps read their rows from global memory
           }
-          if (++s == kCovTcStages) {
+          if (++s == NS) {
             s = 0;
             ph ^= 1u;
           }
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(kCovTcThreads, 1)
         fence_proxy_async();  // generic-proxy B stores -> visible to the tensor core
         tc_fence_before();
         mbar_arrive(&a_full[pb]);
-        if (++s == kCovTcStages) {
+        if (++s == NS) {
           s = 0;
           ph ^= 1u;
         }
