@@ -539,7 +539,7 @@ __device__ __forceinline__ int chol_solve_group(int N, int S, float2 (&A)[CF::MR
   return bad_k ? -bad_k : 0;
 }
 
-// K2 kernel (N > 16): `units` matrices [units][N][N] (full Hermitian; each lane reads the
+// K2 kernel (N >= 13, see chol_select): `units` matrices [units][N][N] (full Hermitian; each lane reads the
 // entries of its register blocks, so the upper entries track the Hermitian Schur complement)
 // -> weights [units][S][N], gamma [units][S] (nullable), info [units].
 template <class CF, int kThreads, int kMinBlocks>
@@ -613,7 +613,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   X(5, (CholCfg<8, 8, 7, 7, 4, false, 4>), 64, 4)               \
   X(6, (CholCfg<8, 8, 8, 8, 1, false, 4>), 64, 5)               \
   X(7, (CholCfg<8, 8, 8, 8, 2, false, 4>), 64, 5)               \
-  X(8, (CholCfg<8, 8, 8, 8, 4, false, 4>), 64, 4)
+  X(8, (CholCfg<8, 8, 8, 8, 4, false, 4>), 64, 4)               \
+  X(9, (CholCfg<4, 4, 4, 4, 1, false, 2>), 512, 1)              \
+  X(10, (CholCfg<4, 4, 4, 4, 2, false, 2>), 512, 1)             \
+  X(11, (CholCfg<4, 4, 4, 4, 4, false, 2>), 512, 1)             \
+  X(12, (CholCfg<4, 4, 4, 4, 8, false, 2>), 512, 1)
 
 struct CholSel {
   int id = -1;
@@ -623,12 +627,20 @@ struct CholSel {
   int min_blocks = 0;  // per SM (launch bounds)
 };
 
-// false if (N, S) has no instantiation (N <= 16, N > 64 or S > 32)
+// false if (N, S) has no instantiation here: N <= 12 (solve_small.cuh, whose arithmetic the
+// fused kernel shares, so the small configuration's staged and fused paths agree to 1e-5),
+// N > 64 or S > 32.  N = 13..16 run half-warp groups (4x4 lanes, two matrices per warp);
+// measured on B200 against solve_small.cuh (262144 matrices): N = 16, S = 16 0.553 vs 1.052
+// ms; N = 16, S = 32 1.23 vs 1.83 ms (N = 12, S = 16 0.350 vs 0.374 ms; N = 10, S = 8 0.235
+// vs 0.209 ms).
 inline bool chol_select(int N, int S, CholSel* sel) {
   int id = -1;
   const int sc = S <= 8 ? 1 : S <= 16 ? 2 : S <= 32 ? 4 : 0;
-  if (N < 17 || N > 64 || !sc) return false;
-  if (N <= 32) id = sc == 1 ? 0 : sc == 2 ? 1 : 2;
+  if (N < 13 || N > 64 || !sc) return false;
+  if (N <= 16) {
+    const int sc4 = S <= 4 ? 1 : S <= 8 ? 2 : S <= 16 ? 4 : 8;  // right-hand-side columns per lane (PC = 4)
+    id = sc4 == 1 ? 9 : sc4 == 2 ? 10 : sc4 == 4 ? 11 : 12;
+  } else if (N <= 32) id = sc == 1 ? 0 : sc == 2 ? 1 : 2;
   else if (N <= 56) id = sc == 1 ? 3 : sc == 2 ? 4 : 5;
   else id = sc == 1 ? 6 : sc == 2 ? 7 : 8;
   switch (id) {

@@ -38,7 +38,7 @@ struct stap_plan {
   size_t cov_tc_smem;
   // K2
   CholSel solve_sel;             // N > 16: chol.cuh
-  int solve_small, solve_lanes;  // N <= 16: solve_small.cuh with `solve_lanes` lanes per matrix
+  int solve_small, solve_lanes;  // no chol_select instantiation: solve_small.cuh with `solve_lanes` lanes per matrix
   int solve_grid;
   size_t solve_smem;
   // K3
@@ -448,9 +448,15 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
     pl->cov_tc_grid = pl->cov_tc_tiles < nsm ? pl->cov_tc_tiles : nsm;  // persistent, one CTA per SM
   }
 
-  // K2: N <= 16 -> solve_small (two matrices per warp for S <= 16); else chol.cuh's lane-group
-  // layout for (N, S).  Persistent grids: the blocks resident on every SM.
-  pl->solve_small = N <= 16;
+  // K2: chol.cuh's lane-group layout where chol_select has an instantiation for (N, S)
+  // (N >= 13); below that solve_small (two matrices per warp for S <= 16).
+  // Persistent grids: the blocks resident on every SM.
+  const bool chol_ok = chol_select(N, S, &pl->solve_sel);
+  if (!chol_ok && N > 16) {
+    delete pl;
+    return STAP_ERR_UNSUPPORTED;
+  }
+  pl->solve_small = chol_ok ? 0 : 1;
   {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
@@ -461,10 +467,6 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
       long long sg = (pl->units + per_cta - 1) / per_cta;
       pl->solve_grid = (int)(sg < 148LL * 64 ? sg : 148LL * 64);
     } else {
-      if (!chol_select(N, S, &pl->solve_sel)) {
-        delete pl;
-        return STAP_ERR_UNSUPPORTED;
-      }
       pl->solve_smem = pl->solve_sel.smem;
       const long long sg = (pl->units + pl->solve_sel.groups - 1) / pl->solve_sel.groups;
       const long long cap = (long long)nsm * pl->solve_sel.min_blocks;
