@@ -1,4 +1,4 @@
-// chol.cuh -- K2 for N > 16: batched Hermitian Cholesky + forward/back solves -> MVDR
+// chol.cuh -- K2 for N >= 13: batched Hermitian Cholesky + forward/back solves -> MVDR
 // weights, one lane group (half warp, warp or warp pair) per matrix, register-resident.
 //
 // Method (include/stap.h; readings c-9, c-10, c-11): R = L L^H, L lower with a real
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 }
 
 // ---- host-side selection ---------------------------------------------------
-// Instantiations (N > 16; N <= 16 runs solve_small.cuh).  Measured on B200 (65536 large /
+// Instantiations (N >= 13; N <= 12 runs solve_small.cuh).  Measured on B200 (65536 large /
 // 131072 medium matrices, S = 16): 4x8 lanes, 14x7 blocks, one 256-thread block per SM (8
 // warps): 1.583 ms (2 x 128: 1.611 ms; 4 x 64: 1.684 ms; old 8x8 two-warp group solver 2.23 ms);
 // N <= 32: 4x8 lanes, 8x4 blocks, one 512-thread block per SM (16 warps, 128 registers):

@@ -13,7 +13,7 @@
 //   3. delta per bin from the lag-0 blocks;
 //   4. solver segments (a lane group per matrix) take bins round-robin: load the
 //      loaded R straight from the lag blocks into registers, Cholesky + solves
-//      (solve_small.cuh for N <= 16, chol.cuh above),
+//      (solve_small.cuh for N = 12 and below, chol.cuh above),
 //      publish w_k in shared [i][SMAX], then apply the S weights to the K cells
 //      of the bin straight from the window (lane = range cell, S accumulators,
 //      broadcast float4 weight reads) and store Y with coalesced 8-byte stores.

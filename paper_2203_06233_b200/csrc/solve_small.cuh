@@ -1,4 +1,5 @@
-// solve_small.cuh -- K2 for N <= 16: Cholesky + forward/back solves, fully
+// solve_small.cuh -- K2 for N <= 16 (the staged path uses it for N <= 12, the fused kernel
+// at N = 4 and 12; chol.cuh takes 13 <= N <= 16): Cholesky + forward/back solves, fully
 // register-resident, compile-time N.
 //
 // Method: as chol.cuh (readings c-9, c-10, c-11).
@@ -133,7 +134,7 @@ __device__ __forceinline__ int small_chol_solve(int S, float2 (&A)[N], const flo
   return segbad ? -(__ffs(segbad)) : 0;
 }
 
-// K2 kernel for N <= 16: `units` matrices [units][N][N] -> weights [units][S][N].
+// K2 kernel (N <= 16): `units` matrices [units][N][N] -> weights [units][S][N].
 template <int N, int LANES>
 __global__ void __launch_bounds__(256, 2) solve_small_kernel(int S, long long units, const float2* __restrict__ cov,
                                                            const float2* __restrict__ steer, float2* __restrict__ wout,

@@ -37,7 +37,7 @@ struct stap_plan {
   CovTcGeom cov_tc_geom;
   size_t cov_tc_smem;
   // K2
-  CholSel solve_sel;             // N > 16: chol.cuh
+  CholSel solve_sel;             // N >= 13: chol.cuh
   int solve_small, solve_lanes;  // no chol_select instantiation: solve_small.cuh with `solve_lanes` lanes per matrix
   int solve_grid;
   size_t solve_smem;
