@@ -617,7 +617,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   X(9, (CholCfg<4, 4, 4, 4, 1, false, 2>), 512, 1)              \
   X(10, (CholCfg<4, 4, 4, 4, 2, false, 2>), 512, 1)             \
   X(11, (CholCfg<4, 4, 4, 4, 4, false, 2>), 512, 1)             \
-  X(12, (CholCfg<4, 4, 4, 4, 8, false, 2>), 512, 1)
+  X(12, (CholCfg<4, 4, 4, 4, 8, false, 2>), 512, 1)             \
+  X(13, (CholCfg<4, 4, 6, 6, 2, false, 2>), 512, 1)             \
+  X(14, (CholCfg<4, 4, 6, 6, 4, false, 2>), 512, 1)
 
 struct CholSel {
   int id = -1;
@@ -629,18 +631,20 @@ struct CholSel {
 
 // false if (N, S) has no instantiation here: N <= 12 (solve_small.cuh, whose arithmetic the
 // fused kernel shares, so the small configuration's staged and fused paths agree to 1e-5),
-// N > 64 or S > 32.  N = 13..16 run half-warp groups (4x4 lanes, two matrices per warp);
-// measured on B200 against solve_small.cuh (262144 matrices): N = 16, S = 16 0.553 vs 1.052
-// ms; N = 16, S = 32 1.23 vs 1.83 ms (N = 12, S = 16 0.350 vs 0.374 ms; N = 10, S = 8 0.235
-// vs 0.209 ms).
+// N > 64 or S > 32.  N = 13..16 (any S) and N = 17..24 with S <= 16 run half-warp groups (4x4
+// lanes, two matrices per warp, the matrix padded to 16 or 24 instead of 32); measured on B200
+// (262144 matrices): N = 16, S = 16 0.553 ms vs 1.052 on solve_small.cuh; N = 16, S = 32 1.23
+// vs 1.83 ms; N = 24, S = 16 1.11 ms vs 1.87 on the 4x8-lane, 32-row layout; N = 20, S = 8
+// 0.61 vs 1.82 ms (N = 12, S = 16 0.350 vs 0.374 ms and N = 10, S = 8 0.235 vs 0.209 ms against
+// solve_small; at N = 17..24, S > 16 the 4x4 lanes spill and the 4x8 layout stays).
 inline bool chol_select(int N, int S, CholSel* sel) {
   int id = -1;
   const int sc = S <= 8 ? 1 : S <= 16 ? 2 : S <= 32 ? 4 : 0;
   if (N < 13 || N > 64 || !sc) return false;
-  if (N <= 16) {
-    const int sc4 = S <= 4 ? 1 : S <= 8 ? 2 : S <= 16 ? 4 : 8;  // right-hand-side columns per lane (PC = 4)
-    id = sc4 == 1 ? 9 : sc4 == 2 ? 10 : sc4 == 4 ? 11 : 12;
-  } else if (N <= 32) id = sc == 1 ? 0 : sc == 2 ? 1 : 2;
+  const int sc4 = S <= 4 ? 1 : S <= 8 ? 2 : S <= 16 ? 4 : 8;  // right-hand-side columns per lane (PC = 4)
+  if (N <= 16) id = sc4 == 1 ? 9 : sc4 == 2 ? 10 : sc4 == 4 ? 11 : 12;
+  else if (N <= 24 && sc4 <= 4) id = sc4 <= 2 ? 13 : 14;
+  else if (N <= 32) id = sc == 1 ? 0 : sc == 2 ? 1 : 2;
   else if (N <= 56) id = sc == 1 ? 3 : sc == 2 ? 4 : 5;
   else id = sc == 1 ? 6 : sc == 2 ? 7 : 8;
   switch (id) {

@@ -459,13 +459,14 @@ def test_run_host_pipelined_batch(stap, name, M):
     dict(C=7, T=9, D=13, R=192, K=64, S=16),   # odd N = 63, ragged tiles
     dict(C=5, T=5, D=67, R=64, K=64, S=16),    # odd N = 25, prime D (wrapped edge tiles)
     dict(C=3, T=9, D=9, R=48, K=16, S=16),     # cov_tc at K = 16, SIMT apply (K % 64 != 0)
-    # every chol.cuh instantiation family: N = 13..16 (4x4 lanes, two matrices per warp),
-    # N = 17 (4x8 lanes, 15 identity rows), S > 16 there, N = 33 with S <= 8 (14x7 blocks, one
+    # every chol.cuh instantiation family: N = 13..24 (4x4 lanes, two matrices per warp),
+    # N = 25..32 (4x8 lanes), S > 16 there, N = 33 with S <= 8 (14x7 blocks, one
     # RHS column per lane), N = 48 with S = 32 (8x8 lanes)
     dict(C=1, T=13, D=15, R=64, K=32, S=8),    # N = 13: the smallest N on chol.cuh
     dict(C=4, T=4, D=9, R=128, K=64, S=16),    # N = 16, S = 16
     dict(C=2, T=7, D=11, R=64, K=32, S=32),    # N = 14, S = 32
-    dict(C=1, T=17, D=19, R=64, K=32, S=3),    # N = 17
+    dict(C=1, T=17, D=19, R=64, K=32, S=3),    # N = 17 (4x4 lanes, 6x6 blocks)
+    dict(C=5, T=5, D=9, R=64, K=32, S=16),     # N = 25: the first N on 4x8 lanes, 8x4 blocks
     dict(C=4, T=5, D=7, R=96, K=48, S=24),     # N = 20, S = 24 (four RHS columns per lane)
     dict(C=3, T=11, D=13, R=128, K=64, S=8),   # N = 33, S = 8
     dict(C=8, T=6, D=9, R=128, K=128, S=32),   # N = 48, S = 32
