@@ -619,7 +619,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   X(11, (CholCfg<4, 4, 4, 4, 4, false, 2>), 512, 1)             \
   X(12, (CholCfg<4, 4, 4, 4, 8, false, 2>), 512, 1)             \
   X(13, (CholCfg<4, 4, 6, 6, 2, false, 2>), 512, 1)             \
-  X(14, (CholCfg<4, 4, 6, 6, 4, false, 2>), 512, 1)
+  X(14, (CholCfg<4, 4, 6, 6, 4, false, 2>), 512, 1)             \
+  X(15, (CholCfg<4, 8, 10, 5, 1, false, 2>), 384, 1)            \
+  X(16, (CholCfg<4, 8, 10, 5, 2, false, 2>), 384, 1)            \
+  X(17, (CholCfg<4, 8, 12, 6, 1, false, 2>), 256, 1)            \
+  X(18, (CholCfg<4, 8, 12, 6, 2, false, 2>), 256, 1)
 
 struct CholSel {
   int id = -1;
@@ -636,7 +640,9 @@ struct CholSel {
 // (262144 matrices): N = 16, S = 16 0.553 ms vs 1.052 on solve_small.cuh; N = 16, S = 32 1.23
 // vs 1.83 ms; N = 24, S = 16 1.11 ms vs 1.87 on the 4x8-lane, 32-row layout; N = 20, S = 8
 // 0.61 vs 1.82 ms (N = 12, S = 16 0.350 vs 0.374 ms and N = 10, S = 8 0.235 vs 0.209 ms against
-// solve_small; at N = 17..24, S > 16 the 4x4 lanes spill and the 4x8 layout stays).
+// solve_small; at N = 17..24, S > 16 the 4x4 lanes spill and the 4x8 layout stays).  Likewise
+// N = 33..40 and 41..48 with S <= 16 get 40- and 48-row layouts instead of 56: N = 48, S = 16
+// 1.25 vs 1.66 ms; N = 40, S = 16 0.76 ms (65536 matrices).
 inline bool chol_select(int N, int S, CholSel* sel) {
   int id = -1;
   const int sc = S <= 8 ? 1 : S <= 16 ? 2 : S <= 32 ? 4 : 0;
@@ -645,6 +651,8 @@ inline bool chol_select(int N, int S, CholSel* sel) {
   if (N <= 16) id = sc4 == 1 ? 9 : sc4 == 2 ? 10 : sc4 == 4 ? 11 : 12;
   else if (N <= 24 && sc4 <= 4) id = sc4 <= 2 ? 13 : 14;
   else if (N <= 32) id = sc == 1 ? 0 : sc == 2 ? 1 : 2;
+  else if (N <= 40 && sc <= 2) id = sc == 1 ? 15 : 16;
+  else if (N <= 48 && sc <= 2) id = sc == 1 ? 17 : 18;
   else if (N <= 56) id = sc == 1 ? 3 : sc == 2 ? 4 : 5;
   else id = sc == 1 ? 6 : sc == 2 ? 7 : 8;
   switch (id) {

@@ -276,7 +276,7 @@ void solve_dispatch(const stap_plan* pl, const float2* cov, const float2* steer,
     solve_small_launch(pl->kp.N, pl->solve_lanes, pl->solve_grid, 256, pl->solve_smem, st, pl->kp.S, pl->units, cov,
                        steer, w, g, info);
   else
-    chol_launch(pl->solve_sel, pl->solve_grid, st, pl->kp.N, pl->kp.S, pl->units, cov, steer, w, g, info);
+    solve_chol_launch(pl->solve_sel, pl->solve_grid, st, pl->kp.N, pl->kp.S, pl->units, cov, steer, w, g, info);
 }
 
 stap_status check_launch() {
@@ -538,7 +538,7 @@ static stap_status plan_create_impl(const stap_params* p, stap_plan** out_plan, 
     if (pl->solve_small)
       solve_small_set_attr(N, pl->solve_lanes, pl->solve_smem);
     else
-      chol_set_attr(pl->solve_sel);
+      solve_chol_set_attr(pl->solve_sel);
     set_apply_attr(pl->apply_smax, pl->apply_smem);
     if (pl->apply_tc)
       apply_tc_attr(N, pl->apply_tc_smem);

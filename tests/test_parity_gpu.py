@@ -468,7 +468,10 @@ def test_run_host_pipelined_batch(stap, name, M):
     dict(C=1, T=17, D=19, R=64, K=32, S=3),    # N = 17 (4x4 lanes, 6x6 blocks)
     dict(C=5, T=5, D=9, R=64, K=32, S=16),     # N = 25: the first N on 4x8 lanes, 8x4 blocks
     dict(C=4, T=5, D=7, R=96, K=48, S=24),     # N = 20, S = 24 (four RHS columns per lane)
-    dict(C=3, T=11, D=13, R=128, K=64, S=8),   # N = 33, S = 8
+    dict(C=3, T=11, D=13, R=128, K=64, S=8),   # N = 33, S = 8 (40-row layout)
+    dict(C=8, T=5, D=9, R=128, K=64, S=16),    # N = 40, S = 16
+    dict(C=7, T=6, D=11, R=64, K=32, S=5),     # N = 42, S = 5 (48-row layout)
+    dict(C=7, T=7, D=9, R=128, K=64, S=16),    # N = 49, S = 16 (56-row layout)
     dict(C=8, T=6, D=9, R=128, K=128, S=32),   # N = 48, S = 32
 ])
 @pytest.mark.parametrize("staged,prec", [(False, "fp32"), (True, "fp32"), (True, "tf32x3")])
